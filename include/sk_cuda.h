@@ -1,0 +1,197 @@
+/* sk_cuda.h — C-ABI of the B200 (sm_100a) stencil-composition hot path.
+ *
+ * The drop-in boundary for the data-parallel half of the reference library
+ * `stencilkit` (/root/reference/proj). Everything is `extern "C"`, plain
+ * pointers and sizes; no C++ or torch types cross it. The reference-facing
+ * C++ wrapper is include/stencilkit/cuda.hpp (same names and argument meaning
+ * as the reference functions it replaces); INTEGRATION.md shows the binding.
+ *
+ * Conventions (mirroring the reference):
+ *  - Every entry point returns an int status: SK_OK (0) or SK_ERR_<Errc>+...,
+ *    the reference `stencilkit::Errc` ordinal + 1 (error.hpp:9-28), or one of
+ *    the CUDA-side codes >= 100. sk_last_error() returns the thread-local
+ *    message of the most recent failure (the reference's Error::what()).
+ *  - Device pointers are caller-owned unless created by an *_create call;
+ *    opaque handles are freed by the matching *_destroy.
+ *  - `stream` may be NULL (legacy default stream) or any cudaStream_t.
+ *  - Functions named *_host take HOST buffers and copy in/out inside the call
+ *    (the reference's std::span signatures); the others take DEVICE pointers.
+ *  - Grids are lexicographic with x fastest (grid.cpp:93-96); on a periodic
+ *    axis every point is an unknown, on a simply-supported or clamped axis
+ *    only the n-2 interior points are (grid.hpp:27-29).
+ *  - All arithmetic is fp64; CSR indices are int64 (reference layout,
+ *    grid.hpp:39-46) or int32 (compact, opt-in).
+ *  - Weights reach the device as coeff.to_double() * pow_int(h, h_power), the
+ *    exact expression of grid.cpp:77-81.
+ */
+#ifndef SK_CUDA_H
+#define SK_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: reference Errc ordinal + 1 (error.hpp:9-28) ---------- */
+enum sk_status {
+  SK_OK = 0,
+  SK_ERR_ZERO_SCALE = 1,
+  SK_ERR_DIM_MISMATCH = 2,
+  SK_ERR_POWER_MISMATCH = 3,
+  SK_ERR_EMPTY_STENCIL = 4,
+  SK_ERR_TRUNCATION_TOO_SMALL = 5,
+  SK_ERR_NOT_NORMALIZED = 6,
+  SK_ERR_ACCURACY_EXCEEDS_TRUNCATION = 7,
+  SK_ERR_MIXED_LEADING_ORDER = 8,
+  SK_ERR_SINGULAR_SYSTEM = 9,
+  SK_ERR_UNSUPPORTED_ACCURACY = 10,
+  SK_ERR_STENCIL_WIDER_THAN_GRID = 11,
+  SK_ERR_SHAPE_MISMATCH = 12,
+  SK_ERR_NO_CONVERGENCE = 13,
+  SK_ERR_NOT_DISSIPATIVE = 14,
+  SK_ERR_UNSTABLE_FOR_ALL_DT = 15,
+  SK_ERR_NON_PERIODIC = 16,
+  SK_ERR_ZERO_DENOMINATOR = 17,
+  SK_ERR_INVALID_ARGUMENT = 18,
+  /* device-side failures (no reference equivalent) */
+  SK_ERR_CUDA = 100,
+  SK_ERR_OUT_OF_MEMORY = 101,
+  SK_ERR_NO_DEVICE = 102
+};
+
+/* Boundary kind per axis. periodic and simply_supported are the reference's
+ * BoundaryKind (grid.hpp:17); clamped (u = du/dn = 0, ghosts by even
+ * reflection) is the extension BASELINE.json configs 2 and 5 require. */
+enum sk_bc { SK_BC_PERIODIC = 0, SK_BC_SIMPLY_SUPPORTED = 1, SK_BC_CLAMPED = 2 };
+
+/* GridSpec (grid.hpp:22-34): n = points per axis INCLUDING boundary points. */
+typedef struct sk_grid_desc {
+  int dim;       /* 1..3 */
+  int64_t n[3];  /* points per axis, boundary included; unused axes ignored */
+  double h;      /* uniform spacing */
+  int bc[3];     /* enum sk_bc per axis */
+} sk_grid_desc;
+
+/* CahnHilliardParams (cahn_hilliard.hpp:14-22), chemistry f'(c) =
+ * 2 rho_w (c - c_alpha)(c - c_beta)(2c - c_alpha - c_beta) (cahn_hilliard.cpp:70-73). */
+typedef struct sk_ch_params {
+  double kappa;
+  double mobility;
+  double rho_w;
+  double c_alpha;
+  double c_beta;
+} sk_ch_params;
+
+/* SolveOptions (linalg.hpp:13-17) */
+typedef struct sk_solve_options {
+  double rel_tol;      /* default 1e-10 */
+  int64_t max_iter;    /* <= 0: 10 * rows, as linalg.cpp:20 */
+  int deflate_mean;    /* nonzero: subtract the mean of x on return */
+  int check_every;     /* device iterations between host status polls (0: 64) */
+} sk_solve_options;
+
+typedef struct sk_solve_report {
+  int64_t iterations;        /* CG iterations executed (linalg.cpp loop counter) */
+  int64_t restarts;          /* true-residual restarts (linalg.cpp:42-46) */
+  double true_rel_residual;  /* ||b - M x|| / ||b|| at return */
+  double recurrence_rel_residual; /* sqrt(rho) / ||b|| at return */
+} sk_solve_report;
+
+typedef struct sk_stencil sk_stencil; /* device-ready composed stencil */
+typedef struct sk_csr sk_csr;         /* device-resident CSR matrix */
+
+/* ---- library ------------------------------------------------------------ */
+const char* sk_last_error(void);
+const char* sk_status_name(int status);
+int sk_version(void);
+/* Select the device for this thread and create its context. */
+int sk_device_init(int device);
+/* Device allocation helpers for callers without their own allocator. */
+int sk_device_alloc(size_t bytes, void** out);
+int sk_device_free(void* p);
+int sk_memcpy_h2d(void* dst_dev, const void* src_host, size_t bytes, void* stream);
+int sk_memcpy_d2h(void* dst_host, const void* src_dev, size_t bytes, void* stream);
+int sk_stream_sync(void* stream);
+/* Host-side seeded input: std::mt19937_64(seed) + uniform_real_distribution<double>(lo, hi),
+ * drawn in order — the generator the reference uses (linalg.cpp:77-78). */
+int sk_fill_uniform_host(uint64_t seed, int64_t count, double lo, double hi, double* out);
+/* Number of kernel launches this library has issued (monotone counter). */
+int64_t sk_launch_count(void);
+
+/* ---- stencil (host composition result -> device) ------------------------
+ * Replaces handing a `stencilkit::Stencil` (stencil.hpp:19-42) to assemble().
+ * offsets: nent*dim ints (entry-major), coeff: the exact coefficients as
+ * doubles (Rational::to_double, rational.hpp:32), h_power: Stencil::h_power(). */
+int sk_stencil_create(int dim, int nent, const int32_t* offsets, const double* coeff, int h_power,
+                      sk_stencil** out);
+int sk_stencil_destroy(sk_stencil* s);
+/* Which kernel the stencil maps to: 0 generic (any offsets), 1 symmetric 2D
+ * radius<=2 (5/13-point), 2 symmetric 3D radius<=2 (7/25-point), 3 symmetric
+ * 3D radius<=4 (73-point family). */
+int sk_stencil_kernel_class(const sk_stencil* s);
+
+/* ---- matrix-free composed apply (no reference symbol; equals
+ * apply(assemble(s, g), u), grid.cpp:166-172) ---------------------------- */
+int sk_composed_apply(const sk_stencil* s, const sk_grid_desc* g, const double* u_dev, double* v_dev,
+                      void* stream);
+/* `repeats` applications of s to the same u, outputs alternating between
+ * v0_dev and v1_dev (BASELINE config 1); captured in one CUDA graph. */
+int sk_composed_apply_repeat(const sk_stencil* s, const sk_grid_desc* g, const double* u_dev,
+                             double* v0_dev, double* v1_dev, int repeats, void* stream);
+int sk_composed_apply_host(const sk_stencil* s, const sk_grid_desc* g, const double* u_host,
+                           double* v_host);
+
+/* ---- fused explicit Cahn-Hilliard step ----------------------------------
+ *   c <- c + dt * M * ( L f'(c) - kappa * B c ),  B = compose(L, L)
+ * L = laplacian(dim, 2) (5/7-point), B its composition (13/25-point), as the
+ * reference stepper builds them (cahn_hilliard.cpp:126-128). Periodic grids
+ * only (cahn_hilliard.cpp:12-16). `lap` and `bilap` are the host-composed
+ * stencils. Ping-pong between c_dev and scratch_dev; *result_is_scratch tells
+ * which holds the final field. */
+int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
+                   const sk_ch_params* p, double dt, int64_t nsteps, double* c_dev,
+                   double* scratch_dev, int* result_is_scratch, void* stream);
+int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
+                        const sk_ch_params* p, double dt, int64_t nsteps, double* c_host);
+/* free_energy (cahn_hilliard.cpp:77-114): h^d sum f_chem + kappa/2 |central grad|^2 */
+int sk_free_energy(const sk_grid_desc* g, const sk_ch_params* p, const double* c_dev,
+                   double* energy_host, void* stream);
+
+/* ---- CSR assembly (grid.cpp:62-158) and SpMV (kernels.cpp:8-17) --------- */
+int sk_csr_assemble(const sk_stencil* s, const sk_grid_desc* g, int index_bits, sk_csr** out,
+                    void* stream);
+int sk_csr_upload(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                  const int64_t* col_idx, const double* values, int index_bits, sk_csr** out);
+int sk_csr_info(const sk_csr* m, int64_t* rows, int64_t* cols, int64_t* nnz, int* index_bits);
+int sk_csr_download(const sk_csr* m, int64_t* row_ptr, int64_t* col_idx, double* values);
+int sk_csr_destroy(sk_csr* m);
+/* y = M x, per-row sequential accumulation in column order (bit-identical to
+ * the reference's serial csr_matvec as built by its CMake Release flags). */
+int sk_csr_matvec(const sk_csr* m, const double* x_dev, double* y_dev, void* stream);
+int sk_csr_matvec_host(const sk_csr* m, const double* x_host, double* y_host);
+
+/* ---- BLAS-1 (kernels.cpp:19-60); deterministic two-level reductions ----- */
+int sk_dot(int64_t n, const double* a_dev, const double* b_dev, double* out_host, void* stream);
+int sk_nrm2(int64_t n, const double* a_dev, double* out_host, void* stream);
+int sk_sum(int64_t n, const double* a_dev, double* out_host, void* stream);
+int sk_minmax(int64_t n, const double* a_dev, double* lo_host, double* hi_host, void* stream);
+int sk_axpy(int64_t n, double a, const double* x_dev, double* y_dev, void* stream);  /* y += a x */
+int sk_xpby(int64_t n, const double* x_dev, double b, double* y_dev, void* stream);  /* y = x + b y */
+
+/* ---- conjugate gradients (linalg.cpp:15-72) ------------------------------
+ * x0 = 0; accepts only when the TRUE residual ||b - M x|| <= rel_tol ||b||,
+ * restarting from x on recurrence drift; SK_ERR_NO_CONVERGENCE when M is not
+ * positive definite on the Krylov space or the budget runs out. x_dev receives
+ * the last iterate even on failure; report may be NULL. */
+int sk_cg_solve(const sk_csr* m, const double* b_dev, double* x_dev, const sk_solve_options* opts,
+                sk_solve_report* report, void* stream);
+int sk_cg_solve_host(const sk_csr* m, const double* b_host, double* x_host,
+                     const sk_solve_options* opts, sk_solve_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SK_CUDA_H */

@@ -1,0 +1,104 @@
+"""Fused explicit Cahn-Hilliard stepping and the free energy on the device.
+
+Mirrors the reference's CahnHilliardParams / CahnHilliardState / free_energy
+(cahn_hilliard.hpp:14-44) with the EXPLICIT forward-Euler step the BASELINE
+configs specify (the reference's stepper is IMEX, cahn_hilliard.cpp:139-189;
+SURVEY.md Appendix A restates the explicit step from its pieces):
+    c <- c + dt M (L f'(c) - kappa B c),  L = laplacian(d, 2), B = compose(L, L)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Tuple
+
+import numpy as np
+
+from ._lib import ChParams, check, ensure_device
+from .device import DeviceArray
+from .errors import Errc, StencilkitError
+from .grid import BoundaryKind, DeviceStencil, GridSpec
+from .stencil import compose, laplacian
+
+
+@dataclass
+class CahnHilliardParams:
+    """cahn_hilliard.hpp:14-22 (defaults are the reference's benchmark values)."""
+    kappa: float = 2.0
+    mobility: float = 5.0
+    rho_w: float = 5.0
+    c_alpha: float = 0.3
+    c_beta: float = 0.7
+
+    @staticmethod
+    def from_epsilon(eps: float) -> "CahnHilliardParams":
+        """u_t = Delta(u^3 - u - eps^2 Delta u): f'(u) = u^3 - u <=> rho_w = 1/4, c_alpha = -1, c_beta = 1."""
+        return CahnHilliardParams(kappa=eps * eps, mobility=1.0, rho_w=0.25, c_alpha=-1.0, c_beta=1.0)
+
+    def c_struct(self) -> ChParams:
+        p = ChParams()
+        p.kappa, p.mobility, p.rho_w, p.c_alpha, p.c_beta = (self.kappa, self.mobility, self.rho_w, self.c_alpha,
+                                                              self.c_beta)
+        return p
+
+
+@dataclass
+class CahnHilliardState:
+    grid: GridSpec
+    c: np.ndarray
+    t: float = 0.0
+    energy_history: List[Tuple[float, float]] = field(default_factory=list)
+
+
+class CahnHilliardExplicit:
+    """Device stepper: L and B composed on the host, one fused kernel per step."""
+
+    def __init__(self, grid: GridSpec, params: CahnHilliardParams):
+        grid.validate()
+        if any(b != BoundaryKind.periodic for b in grid.bc):
+            raise StencilkitError(Errc.non_periodic, "Cahn-Hilliard runs on periodic grids")
+        self.lib = ensure_device()
+        self.grid = grid
+        self.params = params
+        lap = laplacian(grid.dim, 2)
+        self.lap = DeviceStencil(lap)
+        self.bilap = DeviceStencil(compose(lap, lap))
+        self._desc = grid.desc()
+        self._p = params.c_struct()
+
+    def run_device(self, c: DeviceArray, scratch: DeviceArray, dt: float, nsteps: int, stream=None) -> DeviceArray:
+        """nsteps fused steps ping-ponging c <-> scratch; returns the buffer holding the result."""
+        which = C.c_int()
+        check(self.lib.sk_ch_explicit(self.lap.handle, self.bilap.handle, C.byref(self._desc), C.byref(self._p),
+                                      dt, nsteps, c.ptr, scratch.ptr, C.byref(which), stream))
+        return scratch if which.value else c
+
+    def step(self, state: CahnHilliardState, dt: float, nsteps: int = 1) -> None:
+        """Host state in/out (the reference-facing call): copies in, steps, copies out."""
+        if not dt > 0:
+            raise StencilkitError(Errc.invalid_argument, "dt must be positive")
+        c = np.ascontiguousarray(state.c, dtype=np.float64).ravel().copy()
+        if c.size != self.grid.unknown_count():
+            raise StencilkitError(Errc.shape_mismatch, "state does not match the stepper grid")
+        check(self.lib.sk_ch_explicit_host(self.lap.handle, self.bilap.handle, C.byref(self._desc),
+                                           C.byref(self._p), dt, nsteps, c.ctypes.data))
+        state.c = c
+        state.t += dt * nsteps
+
+
+def free_energy(state_or_field, params: CahnHilliardParams, grid: GridSpec | None = None, stream=None) -> float:
+    """h^d sum [f_chem(c) + kappa/2 |central grad c|^2] (cahn_hilliard.cpp:77-114)."""
+    lib = ensure_device()
+    if isinstance(state_or_field, CahnHilliardState):
+        grid = state_or_field.grid
+        dev = DeviceArray.from_host(np.asarray(state_or_field.c, dtype=np.float64).ravel())
+    elif isinstance(state_or_field, DeviceArray):
+        dev = state_or_field
+    else:
+        dev = DeviceArray.from_host(np.asarray(state_or_field, dtype=np.float64).ravel())
+    assert grid is not None
+    d = grid.desc()
+    p = params.c_struct()
+    out = C.c_double()
+    check(lib.sk_free_energy(C.byref(d), C.byref(p), dev.ptr, C.byref(out), stream))
+    return out.value

@@ -1,0 +1,391 @@
+// Conjugate gradients on the device, control flow of linalg.cpp:15-72.
+//
+// Per iteration three kernels (captured in a CUDA graph of `check_every`
+// iterations; all scalars stay on the device, the host polls a status word
+// once per graph):
+//   K1  q = M p (CSR, reference rounding) fused with the p.q partials; the
+//       last CTA forms pq, flags "not positive definite" (linalg.cpp:50-51)
+//       or sets alpha = rho / pq.
+//   K2  x += alpha p ; r -= alpha q (bit-exact axpy) fused with r.r
+//       partials; the last CTA sets rho_next, beta, counts the iteration and
+//       raises CHECK when sqrt(rho) <= tol ||b|| (linalg.cpp:31) or stops at
+//       max_iter.
+//   K3  p = r + beta p (bit-exact xpby).
+// Kernels of a graph become no-ops once the status leaves RUNNING, so the
+// iteration count is exact. The rare true-residual check / restart
+// (linalg.cpp:32-47) and the final acceptance test (:59-66) run outside the
+// graph.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "sk_internal.hpp"
+
+namespace sk {
+
+namespace {
+
+constexpr int kT = 256;
+enum : int { kRunning = 0, kCheck = 1, kNotPD = 2, kMaxIter = 3 };
+
+struct CgState {
+  double rho, pq, alpha, beta, target;
+  double scalar_out;  // result slot of auxiliary reductions
+  int64_t it, max_iter;
+  int status;
+  int pad;
+  unsigned counter[4];
+};
+
+template <class IDX>
+__device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp, const IDX* __restrict__ col,
+                                          const double* __restrict__ val, const double* __restrict__ x, int64_t i) {
+  const int64_t b = __ldg(rp + i), e = __ldg(rp + i + 1);
+  double acc = 0.0;
+  for (int64_t k = b; k < e; ++k) acc = __dadd_rn(acc, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
+  return acc;
+}
+
+template <class IDX>
+__global__ void __launch_bounds__(kT) k1_spmv_pq(int64_t n, const int64_t* __restrict__ rp, const IDX* __restrict__ col,
+                                                 const double* __restrict__ val, const double* __restrict__ p,
+                                                 double* __restrict__ q, CgState* st, double* partials) {
+  if (st->status != kRunning) return;
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    const double qi = row_dot(rp, col, val, p, i);
+    q[i] = qi;
+    acc = fma(p[i], qi, acc);
+  }
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[0])) {
+    const double pq = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->pq = pq;
+      if (pq <= 0) st->status = kNotPD;
+      else st->alpha = st->rho / pq;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT) k2_update_rr(int64_t n, const double* __restrict__ p, const double* __restrict__ q,
+                                                   double* __restrict__ x, double* __restrict__ r, CgState* st,
+                                                   double* partials) {
+  if (st->status != kRunning) return;
+  __shared__ double sh[32];
+  const double alpha = st->alpha, nalpha = -alpha;
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));            // axpy(alpha, p, x)
+    const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, q[i]));  // axpy(-alpha, q, r)
+    r[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[1])) {
+    const double rho_next = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->beta = rho_next / st->rho;
+      st->rho = rho_next;
+      st->it += 1;
+      if (st->it >= st->max_iter) st->status = kMaxIter;
+      else if (sqrt(rho_next) <= st->target) st->status = kCheck;
+    }
+  }
+}
+
+__global__ void k3_xpby(int64_t n, const double* __restrict__ r, double* __restrict__ p, const CgState* st) {
+  if (st->status != kRunning) return;
+  const double beta = st->beta;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+}
+
+// q = M x ; out = sum (b - q)^2   (linalg.cpp:33-39, :59-61)
+template <class IDX>
+__global__ void __launch_bounds__(kT) k_true_residual(int64_t n, const int64_t* __restrict__ rp, const IDX* __restrict__ col,
+                                                      const double* __restrict__ val, const double* __restrict__ x,
+                                                      const double* __restrict__ b, double* __restrict__ q, CgState* st,
+                                                      double* partials) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    const double qi = row_dot(rp, col, val, x, i);
+    q[i] = qi;
+    const double d = __dsub_rn(b[i], qi);
+    acc = fma(d, d, acc);
+  }
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[2])) {
+    const double t = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) st->scalar_out = t;
+  }
+}
+
+// restart: r = b - q ; p = r ; rho = r.r   (linalg.cpp:43-46)
+__global__ void __launch_bounds__(kT) k_restart(int64_t n, const double* __restrict__ b, const double* __restrict__ q,
+                                                double* __restrict__ r, double* __restrict__ p, CgState* st,
+                                                double* partials) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    const double ri = __dsub_rn(b[i], q[i]);
+    r[i] = ri;
+    p[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[3])) {
+    const double t = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->rho = t;
+      st->status = kRunning;
+    }
+  }
+}
+
+// op 0: sum a*a ; 1: sum a  -> st->scalar_out (uses counter[2])
+template <int OP>
+__global__ void __launch_bounds__(kT) k_reduce(int64_t n, const double* __restrict__ a, CgState* st, double* partials) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT)
+    acc = OP == 0 ? fma(a[i], a[i], acc) : acc + a[i];
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[2])) {
+    const double t = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) st->scalar_out = t;
+  }
+}
+
+__global__ void k_shift(int64_t n, double* __restrict__ x, double mean) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    x[i] -= mean;
+}
+
+struct Solver {
+  const sk_csr* m;
+  cudaStream_t stream;
+  int64_t n;
+  int grid;
+  CgState* st = nullptr;  // device
+  double* partials = nullptr;
+  double *r = nullptr, *p = nullptr, *q = nullptr;
+
+  int launch_k1() {
+    if (m->index_bits == 32)
+      k1_spmv_pq<int32_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int32_t*>(m->col), m->val, p, q, st,
+                                                    partials);
+    else
+      k1_spmv_pq<int64_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int64_t*>(m->col), m->val, p, q, st,
+                                                    partials);
+    SK_LAUNCH_CHECK("k1_spmv_pq");
+    return SK_OK;
+  }
+  int true_residual(const double* x, const double* b, double* out) {
+    if (m->index_bits == 32)
+      k_true_residual<int32_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int32_t*>(m->col), m->val, x,
+                                                         b, q, st, partials);
+    else
+      k_true_residual<int64_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int64_t*>(m->col), m->val, x,
+                                                         b, q, st, partials);
+    SK_LAUNCH_CHECK("k_true_residual");
+    SK_CUDA_TRY(cudaMemcpyAsync(out, &st->scalar_out, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    SK_CUDA_TRY(cudaStreamSynchronize(stream));
+    *out = std::sqrt(*out);
+    return SK_OK;
+  }
+  template <int OP>
+  int reduce(const double* a, double* out) {
+    k_reduce<OP><<<grid, kT, 0, stream>>>(n, a, st, partials);
+    SK_LAUNCH_CHECK("k_reduce");
+    SK_CUDA_TRY(cudaMemcpyAsync(out, &st->scalar_out, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    SK_CUDA_TRY(cudaStreamSynchronize(stream));
+    return SK_OK;
+  }
+};
+
+}  // namespace
+
+int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
+             cudaStream_t stream) {
+  if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
+  const int64_t n = m->rows;
+  sk_solve_options opts{1e-10, 0, 0, 0};
+  if (o) opts = *o;
+  const int64_t max_iter = opts.max_iter > 0 ? opts.max_iter : 10 * n;  // linalg.cpp:20
+  const int check_every = opts.check_every > 0 ? opts.check_every : 64;
+  sk_solve_report report{0, 0, 0.0, 0.0};
+  if (rep) *rep = report;
+  if (n == 0) return SK_OK;
+
+  Solver s{m, stream, n};
+  int64_t g = (n + kT - 1) / kT;
+  s.grid = int(g > int64_t(kNumSMs) * 8 ? int64_t(kNumSMs) * 8 : g);
+  const size_t vec = sizeof(double) * size_t(n);
+  char* ws = nullptr;
+  const size_t ws_bytes = 3 * vec + sizeof(double) * size_t(s.grid) + sizeof(CgState) + 256;
+  SK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, stream));
+  struct Free {
+    char* p;
+    cudaStream_t s;
+    ~Free() { cudaFreeAsync(p, s); }
+  } guard{ws, stream};
+  s.r = reinterpret_cast<double*>(ws);
+  s.p = s.r + n;
+  s.q = s.p + n;
+  s.partials = s.q + n;
+  s.st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(s.partials + s.grid) + 127) & ~uintptr_t(127));
+
+  // x = 0, r = p = b (linalg.cpp:22)
+  SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
+  SK_CUDA_TRY(cudaMemcpyAsync(s.r, b, vec, cudaMemcpyDeviceToDevice, stream));
+  SK_CUDA_TRY(cudaMemcpyAsync(s.p, b, vec, cudaMemcpyDeviceToDevice, stream));
+  SK_CUDA_TRY(cudaMemsetAsync(s.st, 0, sizeof(CgState), stream));
+  double bb = 0;
+  if (int e = s.reduce<0>(b, &bb)) return e;
+  const double bnorm = std::sqrt(bb);  // :23
+  if (bnorm == 0.0) return SK_OK;      // :24
+  const double target = opts.rel_tol * bnorm;
+  CgState h{};
+  h.rho = bb;  // rho = r.r with r = b (:27)
+  h.target = target;
+  h.it = 0;
+  h.max_iter = max_iter;
+  h.status = kRunning;
+  SK_CUDA_TRY(cudaMemcpyAsync(s.st, &h, sizeof(CgState), cudaMemcpyHostToDevice, stream));
+
+  // graph of `check_every` iterations
+  cudaGraphExec_t exec = nullptr;
+  {
+    cudaStream_t cap = stream ? stream : capture_stream();
+    cudaStream_t keep = s.stream;
+    s.stream = cap;
+    SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    int st = SK_OK;
+    for (int k = 0; k < check_every && st == SK_OK; ++k) {
+      st = s.launch_k1();
+      if (st == SK_OK) {
+        k2_update_rr<<<s.grid, kT, 0, cap>>>(n, s.p, s.q, x, s.r, s.st, s.partials);
+        k3_xpby<<<s.grid, kT, 0, cap>>>(n, s.r, s.p, s.st);
+      }
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    s.stream = keep;
+    if (st != SK_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  }
+  struct GraphFree {
+    cudaGraphExec_t e;
+    ~GraphFree() {
+      if (e) cudaGraphExecDestroy(e);
+    }
+  } gfree{exec};
+  g_launches -= 3 * check_every;  // capture does not execute
+
+  int64_t restarts = 0;
+  double rho = bb;
+  int64_t it = 0;
+  int status = kRunning;
+  for (;;) {
+    if (it >= max_iter) break;
+    if (std::sqrt(rho) <= target) {
+      // recurrence says converged; accept only if the true residual agrees (:31-47)
+      double true_res = 0;
+      if (int e = s.true_residual(x, b, &true_res)) return e;
+      if (true_res <= target) break;
+      k_restart<<<s.grid, kT, 0, stream>>>(n, b, s.q, s.r, s.p, s.st, s.partials);
+      SK_LAUNCH_CHECK("k_restart");
+      restarts++;
+    }
+    SK_CUDA_TRY(cudaGraphLaunch(exec, stream));
+    g_launches += 3 * check_every;
+    SK_CUDA_TRY(cudaMemcpyAsync(&h, s.st, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
+    SK_CUDA_TRY(cudaStreamSynchronize(stream));
+    it = h.it;
+    rho = h.rho;
+    status = h.status;
+    if (status == kNotPD) {
+      report.iterations = it;
+      report.restarts = restarts;
+      if (rep) *rep = report;
+      return fail(SK_ERR_NO_CONVERGENCE, "matrix is not positive definite on the Krylov space");
+    }
+    if (status == kMaxIter) break;
+    if (status == kCheck) {
+      h.status = kRunning;  // the check itself runs at the loop top
+      SK_CUDA_TRY(cudaMemcpyAsync(&s.st->status, &h.status, sizeof(int), cudaMemcpyHostToDevice, stream));
+    }
+  }
+  // final acceptance on the true residual (:59-66)
+  double res = 0;
+  if (int e = s.true_residual(x, b, &res)) return e;
+  report.iterations = it;
+  report.restarts = restarts;
+  report.true_rel_residual = res / bnorm;
+  report.recurrence_rel_residual = std::sqrt(rho) / bnorm;
+  if (rep) *rep = report;
+  if (res > target)
+    return fail(SK_ERR_NO_CONVERGENCE, "cg stalled after " + std::to_string(it) + " iterations at relative residual " +
+                                           std::to_string(res / bnorm));
+  if (opts.deflate_mean) {  // :67-70
+    double sum = 0;
+    if (int e = s.reduce<1>(x, &sum)) return e;
+    const double mean = sum / double(n);
+    k_shift<<<s.grid, kT, 0, stream>>>(n, x, mean);
+    SK_LAUNCH_CHECK("k_shift");
+    SK_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  return SK_OK;
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int sk_cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
+                void* stream) {
+  if (!m) return fail(SK_ERR_INVALID_ARGUMENT, "null matrix");
+  if (m->rows > 0 && (!b || !x)) return fail(SK_ERR_INVALID_ARGUMENT, "null vector");
+  return cg_solve(m, b, x, o, rep, as_stream(stream));
+}
+
+int sk_cg_solve_host(const sk_csr* m, const double* b_host, double* x_host, const sk_solve_options* o,
+                     sk_solve_report* rep) {
+  if (!m) return fail(SK_ERR_INVALID_ARGUMENT, "null matrix");
+  if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
+  if (m->rows == 0) return SK_OK;
+  const size_t bytes = sizeof(double) * size_t(m->rows);
+  double *b = nullptr, *x = nullptr;
+  SK_CUDA_TRY(cudaMalloc(&b, bytes));
+  cudaError_t e = cudaMalloc(&x, bytes);
+  int st = e == cudaSuccess ? SK_OK : cuda_fail(e, "cudaMalloc");
+  if (st == SK_OK && (e = cudaMemcpy(b, b_host, bytes, cudaMemcpyHostToDevice)) != cudaSuccess) st = cuda_fail(e, "H2D");
+  if (st == SK_OK) st = cg_solve(m, b, x, o, rep, nullptr);
+  // the last iterate is returned even on NoConvergence
+  if ((st == SK_OK || st == SK_ERR_NO_CONVERGENCE)) {
+    cudaError_t e2 = cudaMemcpy(x_host, x, bytes, cudaMemcpyDeviceToHost);
+    if (e2 != cudaSuccess && st == SK_OK) st = cuda_fail(e2, "D2H");
+  }
+  cudaFree(b);
+  if (x) cudaFree(x);
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+// Fused explicit Cahn-Hilliard stepping and the free-energy reduction.
+//
+// Reference pieces restated (no explicit stepper exists in the reference;
+// SURVEY.md Appendix A): the stepper's matrices L = assemble(laplacian(d,2))
+// and B = assemble(compose(L,L)) (cahn_hilliard.cpp:126-128) and its explicit
+// chemistry term M L f'(c) (:146-152). One step is
+//     c <- c + dt M (L f'(c) - kappa B c)
+// computed in ONE pass per point (kernels in sk_stencil_kernels.cuh): the
+// tile of c lands in shared memory, f'(c) is evaluated on the fly for the
+// 5/7-point Laplacian, the 13/25-point composed B is summed by orbits, and
+// the update is written to the ping-pong buffer. 16 B of HBM traffic per
+// point per step (read c, write c').
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <mutex>
+
+#include "sk_internal.hpp"
+#include "sk_stencil_kernels.cuh"
+
+namespace sk {
+
+template <Mode M>
+int launch_2d(const Apply2DArgs& a, cudaStream_t stream);
+template <Mode M, class C>
+int launch_3d(Apply3DArgs a, cudaStream_t stream);
+using C3R2 = Cfg3D<2, 64, 16, 2, 2, 4>;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ---- generic fallback pieces (any L/B the fast path does not cover) ------
+__global__ void chem_kernel(int64_t n, const double* __restrict__ c, double* __restrict__ w, ChemParams p) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    w[i] = chem_prime(c[i], p);
+}
+
+// c' = c + dt M (a - kappa b)   (evaluation order of the restated step)
+__global__ void ch_update_kernel(int64_t n, const double* __restrict__ c, const double* __restrict__ la,
+                                 const double* __restrict__ lb, double dtm, double kappa, double* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = __dadd_rn(c[i], __dmul_rn(dtm, __dsub_rn(la[i], __dmul_rn(kappa, lb[i]))));
+}
+
+// ---- free energy (cahn_hilliard.cpp:77-107), reference evaluation order --
+__global__ void __launch_bounds__(kThreads)
+    energy_kernel(const double* __restrict__ c, int dim, int64_t nx, int64_t ny, int64_t nz, double inv_2h,
+                  double kappa, double rho_w, double c_alpha, double c_beta, double* partials, unsigned* counter,
+                  double* out) {
+  __shared__ double sh[32];
+  const int64_t count = nx * ny * nz;
+  const int64_t stride[3] = {1, nx, nx * ny};
+  const int64_t nn[3] = {nx, ny, nz};
+  double acc = 0.0;
+  for (int64_t idx = int64_t(blockIdx.x) * kThreads + threadIdx.x; idx < count;
+       idx += int64_t(gridDim.x) * kThreads) {
+    const double ci = c[idx];
+    const double a = __dsub_rn(ci, c_alpha), b = __dsub_rn(ci, c_beta);
+    double cell = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(rho_w, a), a), b), b);  // f_chem, :65-68
+    int64_t rem = idx;
+    for (int ax = 0; ax < dim; ++ax) {
+      const int64_t na = nn[ax];
+      const int64_t ia = rem % na;
+      rem /= na;
+      const int64_t up = idx + stride[ax] * ((ia + 1 == na) ? 1 - na : 1);
+      const int64_t dn = idx - stride[ax] * ((ia == 0) ? 1 - na : 1);
+      const double grad = __dmul_rn(__dsub_rn(c[up], c[dn]), inv_2h);
+      cell = __dadd_rn(cell, __dmul_rn(__dmul_rn(__dmul_rn(0.5, kappa), grad), grad));
+    }
+    acc += cell;
+  }
+  acc = block_sum<kThreads>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(counter)) {
+    const double t = reduce_partials<kThreads>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) *out = t;
+  }
+}
+
+bool is_lap_shape(const sk_stencil* s, int dim) {
+  // 5/7-point: only the centre and axis-1 orbits
+  const int want = dim == 2 ? 1 : 2;
+  return s->kclass == want && s->orbit_coeff[2] == 0.0 && s->orbit_coeff[3] == 0.0;
+}
+
+bool is_bilap_shape(const sk_stencil* s, int dim) { return s->kclass == (dim == 2 ? 1 : 2); }
+
+struct ChGraph {
+  std::mutex mu;
+  cudaGraphExec_t exec = nullptr;
+  const void* key_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+  double key_val[16] = {};
+  int steps = 0;
+};
+ChGraph g_ch_graph;
+
+constexpr int kGraphSteps = 100;  // kernels per captured graph (even: buffers return to start)
+
+}  // namespace
+
+// One fused step on the fast path (in -> out).
+static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
+                        double dt, const double* in, double* out, cudaStream_t stream, bool bulk_ok_ptrs) {
+  const double dtm = dt * p->mobility;
+  const double fac_b = -dtm * p->kappa;
+  const double sb = pow_int(g.h, bilap->h_power), sl = pow_int(g.h, lap->h_power);
+  OrbitW wb{};
+  for (int i = 0; i < 8; ++i) wb.w[i] = (bilap->orbit_coeff[i] * sb) * fac_b;
+  const double wl0 = (lap->orbit_coeff[0] * sl) * dtm, wl1 = (lap->orbit_coeff[1] * sl) * dtm;
+  const ChemParams chem{p->rho_w, p->c_alpha, p->c_beta};
+  if (g.dim == 2) {
+    Apply2DArgs a{};
+    a.u = in;
+    a.v = out;
+    a.nx = g.n[0];
+    a.ny = g.n[1];
+    a.w = wb;
+    a.wl0 = wl0;
+    a.wl1 = wl1;
+    a.chem = chem;
+    a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= 64 + 4;
+    return launch_2d<Mode::CahnHilliard>(a, stream);
+  }
+  Apply3DArgs a{};
+  a.u = in;
+  a.v = out;
+  a.nx = g.n[0];
+  a.ny = g.n[1];
+  a.nz = g.n[2];
+  a.w = wb;
+  a.wl0 = wl0;
+  a.wl1 = wl1;
+  a.chem = chem;
+  a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R;
+  return launch_3d<Mode::CahnHilliard, C3R2>(a, stream);
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* gd, const sk_ch_params* p,
+                   double dt, int64_t nsteps, double* c, double* scratch, int* result_is_scratch, void* stream_p) {
+  if (!lap || !bilap || !p) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil or params");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  for (int a = 0; a < g.dim; ++a)
+    if (g.bc[a] != SK_BC_PERIODIC) return fail(SK_ERR_NON_PERIODIC, "Cahn-Hilliard runs on periodic grids");
+  if (g.dim != 2 && g.dim != 3) return fail(SK_ERR_INVALID_ARGUMENT, "Cahn-Hilliard stepping is 2D or 3D");
+  if (int st = check_width(lap, g)) return st;
+  if (int st = check_width(bilap, g)) return st;
+  if (!(dt > 0)) return fail(SK_ERR_INVALID_ARGUMENT, "dt must be positive");
+  if (nsteps < 0) return fail(SK_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
+  if (!c || !scratch || c == scratch) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
+  if (result_is_scratch) *result_is_scratch = int(nsteps % 2);
+  if (nsteps == 0 || g.rows == 0) return SK_OK;
+  cudaStream_t stream = as_stream(stream_p);
+  const bool ptr_ok = ((reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(scratch)) & 15) == 0;
+  const bool fast = is_lap_shape(lap, g.dim) && is_bilap_shape(bilap, g.dim);
+
+  if (!fast) {  // generic: four passes per step
+    const int64_t n = g.rows;
+    double* tmp = nullptr;
+    SK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * size_t(3 * n), stream));
+    double *w = tmp, *la = tmp + n, *lb = tmp + 2 * n;
+    const ChemParams chem{p->rho_w, p->c_alpha, p->c_beta};
+    const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(kNumSMs) * 16));
+    double* bufs[2] = {c, scratch};
+    int st = SK_OK;
+    for (int64_t k = 0; k < nsteps && st == SK_OK; ++k) {
+      const double* in = bufs[k % 2];
+      double* out = bufs[(k + 1) % 2];
+      chem_kernel<<<grid, 256, 0, stream>>>(n, in, w, chem);
+      g_launches++;
+      st = launch_apply(lap, g, w, la, stream);
+      if (st == SK_OK) st = launch_apply(bilap, g, in, lb, stream);
+      if (st == SK_OK) {
+        ch_update_kernel<<<grid, 256, 0, stream>>>(n, in, la, lb, dt * p->mobility, p->kappa, out);
+        g_launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) st = cuda_fail(e, "ch_update_kernel");
+      }
+    }
+    cudaFreeAsync(tmp, stream);
+    return st;
+  }
+
+  // fast path: whole chunks of kGraphSteps fused steps replayed as one graph
+  const int64_t full = (nsteps / kGraphSteps) * kGraphSteps;
+  if (full > 0) {
+    std::lock_guard<std::mutex> lock(g_ch_graph.mu);
+    const double key_val[16] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
+                                double(g.n[0]), double(g.n[1]), double(g.n[2]), double(g.dim),
+                                lap->orbit_coeff[0], lap->orbit_coeff[1], bilap->orbit_coeff[0],
+                                bilap->orbit_coeff[1], bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3]};
+    const void* key_ptr[4] = {c, scratch, lap, bilap};
+    bool hit = g_ch_graph.exec != nullptr;
+    for (int i = 0; i < 4 && hit; ++i) hit = key_ptr[i] == g_ch_graph.key_ptr[i];
+    for (int i = 0; i < 16 && hit; ++i) hit = key_val[i] == g_ch_graph.key_val[i];
+    if (!hit) {
+      if (g_ch_graph.exec) {
+        cudaGraphExecDestroy(g_ch_graph.exec);
+        g_ch_graph.exec = nullptr;
+      }
+      cudaStream_t cap = stream ? stream : capture_stream();
+      SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      int st = SK_OK;
+      for (int k = 0; k < kGraphSteps && st == SK_OK; ++k)
+        st = ch_step_fast(lap, bilap, g, p, dt, (k % 2) ? scratch : c, (k % 2) ? c : scratch, cap, ptr_ok);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(cap, &graph);
+      if (st != SK_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      e = cudaGraphInstantiate(&g_ch_graph.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      for (int i = 0; i < 4; ++i) g_ch_graph.key_ptr[i] = key_ptr[i];
+      for (int i = 0; i < 16; ++i) g_ch_graph.key_val[i] = key_val[i];
+      g_launches -= kGraphSteps;  // capture does not execute; counted per replay below
+    }
+    for (int64_t k = 0; k < full; k += kGraphSteps) {
+      SK_CUDA_TRY(cudaGraphLaunch(g_ch_graph.exec, stream));
+      g_launches += kGraphSteps;
+    }
+  }
+  for (int64_t k = full; k < nsteps; ++k) {
+    // kGraphSteps is even, so after `full` steps the field is back in c
+    const bool from_c = (k % 2) == 0;
+    if (int st = ch_step_fast(lap, bilap, g, p, dt, from_c ? c : scratch, from_c ? scratch : c, stream, ptr_ok))
+      return st;
+  }
+  return SK_OK;
+}
+
+int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* gd, const sk_ch_params* p,
+                        double dt, int64_t nsteps, double* c_host) {
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (!c_host && g.rows > 0) return fail(SK_ERR_INVALID_ARGUMENT, "null host field");
+  const size_t bytes = sizeof(double) * size_t(g.rows);
+  double *c = nullptr, *s = nullptr;
+  SK_CUDA_TRY(cudaMalloc(&c, bytes));
+  cudaError_t e = cudaMalloc(&s, bytes);
+  int st = e == cudaSuccess ? SK_OK : cuda_fail(e, "cudaMalloc");
+  if (st == SK_OK && (e = cudaMemcpy(c, c_host, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    st = cuda_fail(e, "H2D");
+  int in_scratch = 0;
+  if (st == SK_OK) st = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, c, s, &in_scratch, nullptr);
+  if (st == SK_OK && (e = cudaMemcpy(c_host, in_scratch ? s : c, bytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    st = cuda_fail(e, "D2H");
+  cudaFree(c);
+  if (s) cudaFree(s);
+  return st;
+}
+
+int sk_free_energy(const sk_grid_desc* gd, const sk_ch_params* p, const double* c, double* energy, void* stream_p) {
+  if (!p || !energy) return fail(SK_ERR_INVALID_ARGUMENT, "null params/output");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  for (int a = 0; a < g.dim; ++a)
+    if (g.bc[a] != SK_BC_PERIODIC) return fail(SK_ERR_NON_PERIODIC, "Cahn-Hilliard runs on periodic grids");
+  if (!c) return fail(SK_ERR_INVALID_ARGUMENT, "null field");
+  cudaStream_t stream = as_stream(stream_p);
+  int grid = int(std::min<int64_t>((g.rows + 1023) / 1024, int64_t(kNumSMs) * 8));
+  if (grid < 1) grid = 1;
+  double* ws = nullptr;
+  SK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(double) * size_t(grid + 4) + 64, stream));
+  double* out = ws + grid;
+  unsigned* counter = reinterpret_cast<unsigned*>(out + 2);
+  cudaMemsetAsync(counter, 0, sizeof(unsigned), stream);
+  energy_kernel<<<grid, kThreads, 0, stream>>>(c, g.dim, g.n[0], g.n[1], g.n[2], 0.5 / g.h, p->kappa, p->rho_w,
+                                               p->c_alpha, p->c_beta, ws, counter, out);
+  g_launches++;
+  cudaError_t e = cudaGetLastError();
+  double total = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&total, out, sizeof(double), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  cudaFreeAsync(ws, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "energy_kernel");
+  *energy = total * pow_int(g.h, g.dim);  // :106
+  return SK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// Shared plumbing for the sm_100a stencil library: status/error handling,
+// launch accounting, PTX wrappers for the bulk-copy + mbarrier pipeline.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "sk_cuda.h"
+
+namespace sk {
+
+// ---- errors ---------------------------------------------------------------
+void set_error(int status, const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+extern std::atomic<int64_t> g_launches;
+
+#define SK_CUDA_TRY(expr)                                        \
+  do {                                                           \
+    cudaError_t sk_e_ = (expr);                                  \
+    if (sk_e_ != cudaSuccess) return ::sk::cuda_fail(sk_e_, #expr); \
+  } while (0)
+
+// After a kernel launch: count it and surface launch-configuration errors.
+#define SK_LAUNCH_CHECK(name)                                          \
+  do {                                                                 \
+    ::sk::g_launches.fetch_add(1, std::memory_order_relaxed);          \
+    cudaError_t sk_e_ = cudaGetLastError();                            \
+    if (sk_e_ != cudaSuccess) return ::sk::cuda_fail(sk_e_, name);     \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ---- grid helpers ----------------------------------------------------------
+struct GridInfo {
+  int dim;
+  int64_t n[3];   // points per axis incl. boundary
+  int64_t un[3];  // unknowns per axis (grid.cpp:27-29)
+  int bc[3];
+  double h;
+  int64_t rows;
+};
+int grid_info(const sk_grid_desc* g, GridInfo* out);  // validates like GridSpec::validate
+double pow_int(double base, int exp);                  // grid.cpp:10-15, bit-identical
+
+constexpr int kNumSMs = 148;
+
+// ---- device helpers --------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1D bulk async copy global -> shared (TMA engine, SASS UBLKCP), completing
+// `bytes` of transaction count on `bar`. src/dst 16-byte aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Streaming 128-bit global store of two doubles (outputs are not re-read).
+__device__ __forceinline__ void st_cs_f64x2(double* p, double a, double b) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction (fixed tree): result valid in thread 0.
+template <int THREADS>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  static_assert(THREADS % 32 == 0 && THREADS <= 1024, "block size");
+  v = warp_sum(v);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  __syncthreads();  // sh may be reused back to back
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < THREADS / 32 ? sh[lane] : 0.0;
+    v = warp_sum(v);
+  }
+  return v;
+}
+
+// "Last block done" ticket: returns true in every thread of the CTA that
+// finishes last; that CTA then combines the per-CTA partials in index order,
+// so the two-level reduction is deterministic for a given grid size.
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned ticket = atomicAdd(counter, 1u);
+    is_last = ticket == gridDim.x - 1;
+    if (is_last) *counter = 0;  // reset for the next launch
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Sum the per-CTA partials in a fixed order (called by the last CTA only).
+template <int THREADS>
+__device__ __forceinline__ double reduce_partials(const double* partials, int count, double* sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < count; i += THREADS) v += __ldcg(partials + i);
+  return block_sum<THREADS>(v, sh);
+}
+
+__device__ __forceinline__ int64_t wrap_idx(int64_t i, int64_t n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+}  // namespace sk

@@ -1,0 +1,54 @@
+// Host-side internal types shared by the library translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "sk_common.cuh"
+
+// Device-ready stencil: the host composition result in canonical order
+// (std::map<Offset, Rational> order, stencil.hpp:44-57), plus its
+// classification onto one of the specialised symmetric kernels.
+struct sk_stencil {
+  int dim = 0;
+  int nent = 0;
+  int h_power = 0;
+  std::vector<int> off;       // nent * 3, lexicographic entry order, unused axes 0
+  std::vector<double> coeff;  // Rational::to_double of each entry
+  int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};  // Stencil::support per axis
+  int kclass = 0;             // 0 generic, 1 sym2d r<=2, 2 sym3d r<=2, 3 sym3d r<=4
+  double orbit_coeff[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int* d_off = nullptr;       // device copy for the generic kernel / assembly
+  double* d_coeff = nullptr;
+  // cached CUDA graph of sk_composed_apply_repeat
+  cudaGraphExec_t rep_exec = nullptr;
+  const void* rep_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t rep_n[3] = {0, 0, 0};
+  int rep_repeats = 0;
+  ~sk_stencil();
+};
+
+// Device-resident CSR (grid.hpp:39-46 layout; int32 columns opt-in).
+struct sk_csr {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int index_bits = 64;
+  int64_t* row_ptr = nullptr;
+  void* col = nullptr;
+  double* val = nullptr;
+  ~sk_csr();
+};
+
+namespace sk {
+
+// Width checks of assemble (grid.cpp:66-75), shared by apply and assembly.
+int check_width(const sk_stencil* s, const GridInfo& g);
+
+// Launch one matrix-free application on `stream` (device pointers).
+int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream);
+
+// Internal stream for graph capture when the caller passes the legacy stream.
+cudaStream_t capture_stream();
+
+}  // namespace sk

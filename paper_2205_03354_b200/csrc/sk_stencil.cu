@@ -1,0 +1,365 @@
+// Stencil handles, orbit classification and the matrix-free composed apply.
+//
+// Reference boundary: the reference has no matrix-free apply; its composed
+// apply is assemble + csr_matvec (grid.cpp:166-172). sk_composed_apply
+// computes the same v = S u without materialising the matrix.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "sk_internal.hpp"
+#include "sk_stencil_kernels.cuh"
+
+sk_stencil::~sk_stencil() {
+  if (rep_exec) cudaGraphExecDestroy(rep_exec);
+  if (d_off) cudaFree(d_off);
+  if (d_coeff) cudaFree(d_coeff);
+}
+
+namespace sk {
+
+namespace {
+
+using Key = std::array<int, 3>;
+
+Key orbit_key(const int* o) {
+  Key k{std::abs(o[0]), std::abs(o[1]), std::abs(o[2])};
+  std::sort(k.begin(), k.end(), std::greater<int>());
+  return k;
+}
+
+// number of distinct signed axis permutations of key living in `dim` axes
+int orbit_size(const Key& key, int dim) {
+  std::set<std::array<int, 3>> seen;
+  std::array<int, 3> perm = {0, 1, 2};
+  do {
+    for (int sgn = 0; sgn < 8; ++sgn) {
+      std::array<int, 3> v{};
+      bool ok = true;
+      for (int a = 0; a < 3; ++a) {
+        int x = key[perm[a]];
+        if (sgn & (1 << a)) x = -x;
+        if (a >= dim && x != 0) ok = false;
+        v[a] = x;
+      }
+      if (ok) seen.insert(v);
+    }
+  } while (std::next_permutation(perm.begin(), perm.end()));
+  return static_cast<int>(seen.size());
+}
+
+const std::vector<Key>& class_orbits(int kclass) {
+  static const std::vector<Key> c1 = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {2, 0, 0}};
+  static const std::vector<Key> c3 = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {2, 0, 0},
+                                      {2, 1, 0}, {2, 2, 0}, {3, 0, 0}, {4, 0, 0}};
+  return kclass == 3 ? c3 : c1;  // classes 1 and 2 share the radius-2 orbit list
+}
+
+// Map the stencil onto a specialised symmetric kernel when every orbit is
+// complete and carries a single coefficient; otherwise generic.
+void classify(sk_stencil* s) {
+  s->kclass = 0;
+  if (s->dim < 2) return;
+  std::map<Key, std::pair<double, int>> orbits;
+  for (int e = 0; e < s->nent; ++e) {
+    const Key k = orbit_key(&s->off[3 * e]);
+    auto it = orbits.find(k);
+    if (it == orbits.end()) {
+      orbits[k] = {s->coeff[e], 1};
+    } else {
+      if (std::memcmp(&it->second.first, &s->coeff[e], sizeof(double)) != 0) return;  // not symmetric
+      it->second.second++;
+    }
+  }
+  for (const auto& [k, v] : orbits)
+    if (v.second != orbit_size(k, s->dim)) return;  // incomplete orbit
+  const std::vector<int> candidates = s->dim == 2 ? std::vector<int>{1} : std::vector<int>{2, 3};
+  for (int kc : candidates) {
+    const auto& list = class_orbits(kc);
+    bool all_in = true;
+    for (const auto& [k, v] : orbits)
+      if (std::find(list.begin(), list.end(), k) == list.end()) all_in = false;
+    if (!all_in) continue;
+    s->kclass = kc;
+    for (size_t i = 0; i < list.size(); ++i) {
+      auto it = orbits.find(list[i]);
+      s->orbit_coeff[i] = it == orbits.end() ? 0.0 : it->second.first;
+    }
+    return;
+  }
+}
+
+template <class K>
+int set_smem(K kernel, int bytes) {
+  if (bytes > 48 * 1024) SK_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return SK_OK;
+}
+
+}  // namespace
+
+cudaStream_t capture_stream() {
+  thread_local cudaStream_t s = nullptr;
+  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  return s;
+}
+
+int check_width(const sk_stencil* s, const GridInfo& g) {
+  if (s->dim != g.dim) return fail(SK_ERR_DIM_MISMATCH, "stencil/grid dimension mismatch");
+  for (int a = 0; a < g.dim; ++a) {
+    if (g.bc[a] == SK_BC_PERIODIC) {
+      if (s->hi[a] - s->lo[a] > g.n[a] - 1)
+        return fail(SK_ERR_STENCIL_WIDER_THAN_GRID, "periodic axis narrower than stencil support");
+    } else if (std::max(std::abs(s->lo[a]), std::abs(s->hi[a])) > g.n[a] - 2) {
+      return fail(SK_ERR_STENCIL_WIDER_THAN_GRID, "reflected ghost would leave the grid");
+    }
+  }
+  return SK_OK;
+}
+
+// ---- kernel configurations ----------------------------------------------
+using T2 = Tile2D<64, 32, 2, 4>;
+using C3R2 = Cfg3D<2, 64, 16, 2, 2, 4>;
+using C3R4 = Cfg3D<4, 64, 16, 2, 2, 4>;
+constexpr int kChunkZ = 32;
+
+template <Mode M>
+int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
+  auto kern = stencil2d_kernel<M, 64, 32, 2, 4>;
+  static int once = set_smem(kern, T2::SMEM_BYTES);
+  if (once != SK_OK) return once;
+  dim3 grid(unsigned((a.nx + 63) / 64), unsigned((a.ny + 31) / 32));
+  kern<<<grid, T2::THREADS, T2::SMEM_BYTES, stream>>>(a);
+  SK_LAUNCH_CHECK("stencil2d_kernel");
+  return SK_OK;
+}
+
+template <Mode M, class C>
+int launch_3d(Apply3DArgs a, cudaStream_t stream) {
+  auto kern = stencil3d_kernel<M, C>;
+  static int once = set_smem(kern, C::SMEM_BYTES);
+  if (once != SK_OK) return once;
+  a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
+  const int tiles_y = int((a.ny + C::TY - 1) / C::TY);
+  a.cz = kChunkZ;
+  dim3 grid(unsigned(a.tiles_x * tiles_y), unsigned((a.nz + a.cz - 1) / a.cz));
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(a);
+  SK_LAUNCH_CHECK("stencil3d_kernel");
+  return SK_OK;
+}
+
+template int launch_2d<Mode::CahnHilliard>(const Apply2DArgs&, cudaStream_t);
+template int launch_3d<Mode::CahnHilliard, C3R2>(Apply3DArgs, cudaStream_t);
+
+int launch_generic(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream) {
+  GenericArgs a{};
+  a.u = u;
+  a.v = v;
+  a.off = s->d_off;
+  a.coeff = s->d_coeff;
+  a.nent = s->nent;
+  a.dim = g.dim;
+  for (int d = 0; d < 3; ++d) {
+    a.n[d] = g.n[d];
+    a.un[d] = g.un[d];
+    a.bc[d] = g.bc[d];
+  }
+  a.scale = pow_int(g.h, s->h_power);
+  a.rows = g.rows;
+  if (g.rows == 0) return SK_OK;
+  const int threads = 256;
+  stencil_generic_kernel<<<unsigned((g.rows + threads - 1) / threads), threads, 0, stream>>>(a);
+  SK_LAUNCH_CHECK("stencil_generic_kernel");
+  return SK_OK;
+}
+
+static bool all_periodic(const GridInfo& g) {
+  for (int a = 0; a < g.dim; ++a)
+    if (g.bc[a] != SK_BC_PERIODIC) return false;
+  return true;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream) {
+  const double scale = pow_int(g.h, s->h_power);
+  OrbitW w{};
+  for (int i = 0; i < 8; ++i) w.w[i] = s->orbit_coeff[i] * scale;  // == coeff.to_double()*pow_int (grid.cpp:80)
+  if (s->kclass == 1 && g.dim == 2 && all_periodic(g)) {
+    Apply2DArgs a{};
+    a.u = u;
+    a.v = v;
+    a.nx = g.n[0];
+    a.ny = g.n[1];
+    a.w = w;
+    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= 64 + 4 && aligned16(u) && aligned16(v);
+    return launch_2d<Mode::Apply>(a, stream);
+  }
+  if ((s->kclass == 2 || s->kclass == 3) && g.dim == 3 && all_periodic(g)) {
+    Apply3DArgs a{};
+    a.u = u;
+    a.v = v;
+    a.nx = g.n[0];
+    a.ny = g.n[1];
+    a.nz = g.n[2];
+    a.w = w;
+    if (s->kclass == 2) {
+      a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && aligned16(u) && aligned16(v);
+      return launch_3d<Mode::Apply, C3R2>(a, stream);
+    }
+    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && aligned16(u) && aligned16(v);
+    return launch_3d<Mode::Apply, C3R4>(a, stream);
+  }
+  return launch_generic(s, g, u, v, stream);
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int sk_stencil_create(int dim, int nent, const int32_t* offsets, const double* coeff, int h_power,
+                      sk_stencil** out) {
+  if (!out) return fail(SK_ERR_INVALID_ARGUMENT, "null output handle");
+  *out = nullptr;
+  if (dim < 1 || dim > 3) return fail(SK_ERR_INVALID_ARGUMENT, "stencil dimension must be 1..3");
+  if (nent < 0 || (nent > 0 && (!offsets || !coeff))) return fail(SK_ERR_INVALID_ARGUMENT, "bad entry arrays");
+  // canonical form (stencil.cpp:15-28): lexicographic offsets, no zeros, never empty
+  std::map<std::array<int, 3>, double> entries;
+  for (int e = 0; e < nent; ++e) {
+    std::array<int, 3> o{0, 0, 0};
+    for (int a = 0; a < dim; ++a) o[a] = offsets[e * dim + a];
+    if (entries.count(o)) return fail(SK_ERR_INVALID_ARGUMENT, "duplicate stencil offset");
+    if (coeff[e] != 0.0) entries[o] = coeff[e];
+  }
+  if (entries.empty())
+    return fail(SK_ERR_EMPTY_STENCIL, "all coefficients cancelled; empty stencil is not representable");
+  auto* s = new sk_stencil;
+  s->dim = dim;
+  s->h_power = h_power;
+  s->nent = static_cast<int>(entries.size());
+  bool first = true;
+  for (const auto& [o, c] : entries) {
+    for (int a = 0; a < 3; ++a) {
+      s->off.push_back(o[a]);
+      if (first) {
+        s->lo[a] = s->hi[a] = o[a];
+      } else {
+        s->lo[a] = std::min(s->lo[a], o[a]);
+        s->hi[a] = std::max(s->hi[a], o[a]);
+      }
+    }
+    s->coeff.push_back(c);
+    first = false;
+  }
+  classify(s);
+  cudaError_t e1 = cudaMalloc(&s->d_off, sizeof(int) * s->off.size());
+  cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&s->d_coeff, sizeof(double) * s->coeff.size()) : e1;
+  if (e2 == cudaSuccess) e2 = cudaMemcpy(s->d_off, s->off.data(), sizeof(int) * s->off.size(), cudaMemcpyHostToDevice);
+  if (e2 == cudaSuccess)
+    e2 = cudaMemcpy(s->d_coeff, s->coeff.data(), sizeof(double) * s->coeff.size(), cudaMemcpyHostToDevice);
+  if (e2 != cudaSuccess) {
+    delete s;
+    return cuda_fail(e2, "sk_stencil_create upload");
+  }
+  *out = s;
+  return SK_OK;
+}
+
+int sk_stencil_destroy(sk_stencil* s) {
+  delete s;
+  return SK_OK;
+}
+
+int sk_stencil_kernel_class(const sk_stencil* s) { return s ? s->kclass : -1; }
+
+int sk_composed_apply(const sk_stencil* s, const sk_grid_desc* gd, const double* u, double* v, void* stream) {
+  if (!s) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (int st = check_width(s, g)) return st;
+  if (g.rows > 0 && (!u || !v)) return fail(SK_ERR_INVALID_ARGUMENT, "null field pointer");
+  if (u == v) return fail(SK_ERR_INVALID_ARGUMENT, "apply cannot run in place");
+  return launch_apply(s, g, u, v, as_stream(stream));
+}
+
+int sk_composed_apply_repeat(const sk_stencil* s_c, const sk_grid_desc* gd, const double* u, double* v0,
+                             double* v1, int repeats, void* stream_p) {
+  auto* s = const_cast<sk_stencil*>(s_c);
+  if (!s) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (int st = check_width(s, g)) return st;
+  if (repeats < 0) return fail(SK_ERR_INVALID_ARGUMENT, "repeats must be >= 0");
+  if (repeats == 0 || g.rows == 0) return SK_OK;
+  if (!u || !v0 || !v1 || u == v0 || u == v1) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
+  cudaStream_t stream = as_stream(stream_p);
+  const bool hit = s->rep_exec && s->rep_key[0] == u && s->rep_key[1] == v0 && s->rep_key[2] == v1 &&
+                   s->rep_repeats == repeats && s->rep_n[0] == g.n[0] && s->rep_n[1] == g.n[1] &&
+                   s->rep_n[2] == g.n[2] && s->rep_key[3] == reinterpret_cast<const void*>(
+                                                               static_cast<uintptr_t>(gd->bc[0] | gd->bc[1] << 2 |
+                                                                                      gd->bc[2] << 4 | 1 << 8));
+  if (!hit) {
+    if (s->rep_exec) {
+      cudaGraphExecDestroy(s->rep_exec);
+      s->rep_exec = nullptr;
+    }
+    cudaStream_t cap = stream ? stream : capture_stream();
+    SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    int st = SK_OK;
+    for (int r = 0; r < repeats && st == SK_OK; ++r) st = launch_apply(s, g, u, (r % 2) ? v1 : v0, cap);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    if (st != SK_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&s->rep_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    s->rep_key[0] = u;
+    s->rep_key[1] = v0;
+    s->rep_key[2] = v1;
+    s->rep_key[3] = reinterpret_cast<const void*>(
+        static_cast<uintptr_t>(gd->bc[0] | gd->bc[1] << 2 | gd->bc[2] << 4 | 1 << 8));
+    s->rep_repeats = repeats;
+    for (int a = 0; a < 3; ++a) s->rep_n[a] = g.n[a];
+  } else {
+    g_launches.fetch_add(repeats);  // the graph replays `repeats` kernels
+  }
+  SK_CUDA_TRY(cudaGraphLaunch(s->rep_exec, stream));
+  return SK_OK;
+}
+
+int sk_composed_apply_host(const sk_stencil* s, const sk_grid_desc* gd, const double* u_host, double* v_host) {
+  if (!s) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (int st = check_width(s, g)) return st;
+  if (g.rows == 0) return SK_OK;
+  if (!u_host || !v_host) return fail(SK_ERR_INVALID_ARGUMENT, "null host buffer");
+  const size_t bytes = sizeof(double) * size_t(g.rows);
+  double *du = nullptr, *dv = nullptr;
+  SK_CUDA_TRY(cudaMalloc(&du, bytes));
+  cudaError_t e = cudaMalloc(&dv, bytes);
+  int st = SK_OK;
+  if (e != cudaSuccess) st = cuda_fail(e, "cudaMalloc");
+  if (st == SK_OK && (e = cudaMemcpy(du, u_host, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    st = cuda_fail(e, "H2D");
+  if (st == SK_OK) st = launch_apply(s, g, du, dv, nullptr);
+  if (st == SK_OK && (e = cudaMemcpy(v_host, dv, bytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    st = cuda_fail(e, "D2H");
+  cudaFree(du);
+  if (dv) cudaFree(dv);
+  return st;
+}
+
+}  // extern "C"

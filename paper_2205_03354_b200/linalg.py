@@ -1,0 +1,69 @@
+"""Device CG with the reference's contract (linalg.hpp:13-23, linalg.cpp:15-72)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import SolveOptionsC, SolveReportC, check
+from .device import DeviceArray
+from .errors import Errc, StencilkitError
+from .grid import CsrMatrix
+
+
+@dataclass
+class SolveOptions:
+    rel_tol: float = 1e-10
+    max_iter: int = 0          # 0: 10 * unknown count
+    deflate_mean: bool = False
+    check_every: int = 64      # device iterations per host status poll
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    restarts: int = 0
+    true_rel_residual: float = 0.0
+    recurrence_rel_residual: float = 0.0
+
+
+def _opts(o: SolveOptions) -> SolveOptionsC:
+    c = SolveOptionsC()
+    c.rel_tol = o.rel_tol
+    c.max_iter = o.max_iter
+    c.deflate_mean = 1 if o.deflate_mean else 0
+    c.check_every = o.check_every
+    return c
+
+
+def cg_solve(m: CsrMatrix, b, opts: SolveOptions | None = None, report: SolveReport | None = None,
+             x_out: DeviceArray | None = None, stream=None):
+    """Solve M x = b. Host b -> host x (numpy); DeviceArray b -> DeviceArray x.
+
+    Raises StencilkitError(no_convergence) exactly when the reference throws
+    (non-PD Krylov space, or true residual above tol after the budget)."""
+    opts = opts or SolveOptions()
+    if m.rows != m.cols:
+        raise StencilkitError(Errc.shape_mismatch, "cg_solve needs a square matrix")
+    rep = SolveReportC()
+    o = _opts(opts)
+    try:
+        if isinstance(b, DeviceArray):
+            if b.count != m.rows:
+                raise StencilkitError(Errc.shape_mismatch, "rhs length does not match matrix")
+            x = x_out if x_out is not None else DeviceArray(m.rows)
+            check(m.lib.sk_cg_solve(m.handle, b.ptr, x.ptr, C.byref(o), C.byref(rep), stream))
+            return x
+        bs = np.ascontiguousarray(np.asarray(b, dtype=np.float64).ravel())
+        if bs.size != m.rows:
+            raise StencilkitError(Errc.shape_mismatch, "rhs length does not match matrix")
+        x = np.empty_like(bs)
+        check(m.lib.sk_cg_solve_host(m.handle, bs.ctypes.data, x.ctypes.data, C.byref(o), C.byref(rep)))
+        return x
+    finally:
+        if report is not None:
+            report.iterations = rep.iterations
+            report.restarts = rep.restarts
+            report.true_rel_residual = rep.true_rel_residual
+            report.recurrence_rel_residual = rep.recurrence_rel_residual
