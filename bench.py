@@ -1,0 +1,516 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 stencil-composition hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+Headline workload (default `ch3d`, BASELINE config 4): the fused explicit
+Cahn-Hilliard step on a periodic 256^3 fp64 grid (7-point Laplacian on
+f'(u) + composed 25-point biharmonic), one step = one pass over the grid,
+metric "CH steps/s". The working set (2 x 134 MB) is larger than the 126 MB
+L2, so every step streams from HBM. `extra` carries the other configs' hot
+paths (config 1 composed apply Gpts/s, config 3 2D CH steps/s, the 73-point
+apply, config 5 CSR assembly + SpMV, config 2 CG iteration rate), each with
+its roofline.
+
+value  : device throughput with the field resident in HBM, CUDA events on
+         the launching stream, K steps between a barrier + sync on both sides,
+         max over ranks (N > 1 runs N independent replicas: "replicas only").
+e2e    : the same K steps through the reference-facing host call
+         (sk_ch_explicit_host: H2D of the field from pinned memory, K steps,
+         D2H of the result), wall-clock around the synchronous call.
+roofline: algorithmic bytes per launch (16 B per grid point: read c, write c')
+         / average launch duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline / --impl reference: the reference library itself
+         (oracle/_ref/libstencilkit_ref.so: unmodified reference sources) on
+         the host cores, the restated explicit step (2 csr_matvec + 2 OpenMP
+         loops).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ------------------------------------------------------------------ helpers --
+def peak_hbm() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if not self.path or not os.path.exists(self.path):
+            return out
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(smax), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+class Dist:
+    """One process per GPU (torchrun); N > 1 is replicas only (no data-path collective)."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+            self.torch = torch
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+class Events:
+    def __init__(self, lib):
+        self.lib = lib
+        self.a, self.b = C.c_void_p(), C.c_void_p()
+        lib.sk_event_create(C.byref(self.a))
+        lib.sk_event_create(C.byref(self.b))
+
+    def start(self, stream=None):
+        self.lib.sk_event_record(self.a, stream)
+
+    def stop_ms(self, stream=None) -> float:
+        self.lib.sk_event_record(self.b, stream)
+        ms = C.c_float()
+        self.lib.sk_event_elapsed_ms(self.a, self.b, C.byref(ms))
+        return float(ms.value)
+
+
+def ncu_traffic(kernel_key: str):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        v = d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        return float(v) if v else None
+    except Exception:
+        return None
+
+
+# -------------------------------------------------------------- workloads --
+def ch_setup(dim: int):
+    """Configs 3 (2D, 2048^2, eps 0.01, seed 1) and 4 (3D, 256^3, eps 0.02, seed 2)."""
+    from paper_2205_03354_b200.cahn_hilliard import CahnHilliardParams
+
+    if dim == 2:
+        n, eps, seed, frac, lap_w = 2048, 0.01, 1, 0.25, 64.0
+    else:
+        n, eps, seed, frac, lap_w = 256, 0.02, 2, 0.2, 144.0
+    h = 1.0 / n
+    p = CahnHilliardParams.from_epsilon(eps)
+    dt = frac * h ** 4 / (lap_w * eps * eps)
+    return n, h, p, dt, seed
+
+
+def field(seed: int, count: int, amp: float = 0.05) -> np.ndarray:
+    from paper_2205_03354_b200._lib import load
+
+    out = np.empty(count)
+    load().sk_fill_uniform_host(seed, count, -1.0, 1.0, out.ctypes.data)
+    return amp * out
+
+
+def run_ch(lib, dim: int, steps: int, warmup: int, d: Dist, e2e: bool = True):
+    from paper_2205_03354_b200.cahn_hilliard import CahnHilliardExplicit
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.grid import make_periodic_grid
+
+    n, h, p, dt, seed = ch_setup(dim)
+    g = make_periodic_grid(dim, n, h)
+    points = g.unknown_count()
+    c0 = field(seed, points)
+    stepper = CahnHilliardExplicit(g, p)
+    c, s = DeviceArray.from_host(c0), DeviceArray(points)
+    for _ in range(max(1, warmup)):
+        stepper.run_device(c, s, dt, 1)
+    stepper.run_device(c, s, dt, steps)  # builds/caches the graph; keeps parity of buffers irrelevant
+    lib.sk_stream_sync(None)
+    ev = Events(lib)
+    d.barrier()
+    lib.sk_stream_sync(None)
+    l0 = lib.sk_launch_count()
+    with ClockSampler(d.local) as clk:
+        ev.start()
+        stepper.run_device(c, s, dt, steps)
+        ms = ev.stop_ms()
+    launches = lib.sk_launch_count() - l0
+    lib.sk_stream_sync(None)
+    d.barrier()
+    ms = d.max(ms)
+    res = {"points": points, "ms": ms, "launches": launches, "clocks": clk.summary(), "n": n, "dt": dt}
+    if e2e:
+        host = np.ascontiguousarray(c0.copy())
+        lib.sk_host_register(host.ctypes.data, host.nbytes)
+        from paper_2205_03354_b200.cahn_hilliard import CahnHilliardState
+
+        st = CahnHilliardState(g, host)
+        stepper.step(st, dt, 1)  # warm the host path
+        st.c = host
+        d.barrier()
+        t0 = time.perf_counter()
+        from paper_2205_03354_b200._lib import check
+
+        check(lib.sk_ch_explicit_host(stepper.lap.handle, stepper.bilap.handle, C.byref(stepper._desc),
+                                      C.byref(stepper._p), dt, steps, host.ctypes.data))
+        e2e_s = d.max(time.perf_counter() - t0)
+        lib.sk_host_unregister(host.ctypes.data)
+        res["e2e_s"] = e2e_s
+        res["e2e_bytes"] = host.nbytes
+    return res
+
+
+def extra_apply2d(lib):
+    """Config 1: 13-point composed biharmonic, 1024^2 periodic, 100 applications (one CUDA graph)."""
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.grid import DeviceStencil, composed_apply_repeat, make_periodic_grid
+    from paper_2205_03354_b200.stencil import bilaplacian
+
+    n, reps = 1024, 100
+    g = make_periodic_grid(2, n, 1.0 / n)
+    s = DeviceStencil(bilaplacian(2))
+    x = np.arange(n) / n
+    u0 = np.outer(np.sin(2 * np.pi * x), np.sin(2 * np.pi * x)).ravel() + 1e-3 * field(0, n * n, 1.0)
+    u, v0, v1 = DeviceArray.from_host(u0), DeviceArray(n * n), DeviceArray(n * n)
+    for _ in range(3):
+        composed_apply_repeat(s, g, u, v0, v1, reps)
+    ev = Events(lib)
+    times = []
+    for _ in range(5):
+        lib.sk_l2_flush(None)
+        ev.start()
+        composed_apply_repeat(s, g, u, v0, v1, reps)
+        times.append(ev.stop_ms())
+    ms = statistics.median(times)
+    pts = reps * n * n
+    gbs = 16.0 * pts / (ms * 1e-3) / 1e9
+    return {"config": "1: 13-pt apply 1024^2 x100 (graph)", "value": pts / (ms * 1e-3) / 1e9, "unit": "Gpts/s",
+            "ms_per_100": ms, "achieved_gbs": gbs, "note": "8.4 MB field: L2-resident across the 100 applications; "
+            "L2 flushed before each timed batch"}
+
+
+def extra_apply3d(lib, which: str):
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.grid import DeviceStencil, composed_apply, make_periodic_grid
+    from paper_2205_03354_b200.stencil import bilaplacian
+
+    n = 256
+    acc = 4 if which == "73" else 2
+    g = make_periodic_grid(3, n, 1.0 / n)
+    s = DeviceStencil(bilaplacian(3, acc))
+    u, v = DeviceArray.from_host(field(5, n ** 3, 1.0)), DeviceArray(n ** 3)
+    for _ in range(3):
+        composed_apply(s, g, u, out=v)
+    ev = Events(lib)
+    reps = 20
+    lib.sk_stream_sync(None)
+    ev.start()
+    for _ in range(reps):
+        composed_apply(s, g, u, out=v)
+    ms = ev.stop_ms() / reps
+    pts = n ** 3
+    return {"config": f"{which}-pt composed apply 256^3 periodic", "value": pts / (ms * 1e-3) / 1e9,
+            "unit": "Gpts/s", "ms_per_apply": ms, "achieved_gbs": 16.0 * pts / (ms * 1e-3) / 1e9}
+
+
+def extra_csr73(lib, bits: int):
+    """Config 5 at 256 intervals (255^3 rows, 73-point clamped): GPU assembly + SpMV."""
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, assemble, make_grid
+    from paper_2205_03354_b200.kernels import csr_matvec
+    from paper_2205_03354_b200.stencil import bilaplacian
+
+    N = 256
+    g = make_grid(3, N + 1, 1.0 / N, BoundaryKind.clamped)
+    s = DeviceStencil(bilaplacian(3, 4))
+    ev = Events(lib)
+    ev.start()
+    m = assemble(s, g, index_bits=bits)
+    asm_ms = ev.stop_ms()
+    rows, nnz = m.rows, m.nnz()
+    x, y = DeviceArray.from_host(field(11, rows, 1.0)), DeviceArray(rows)
+    for _ in range(3):
+        csr_matvec(m, x, y)
+    reps = 10
+    lib.sk_stream_sync(None)
+    ev.start()
+    for _ in range(reps):
+        csr_matvec(m, x, y)
+    ms = ev.stop_ms() / reps
+    idx = bits // 8
+    spmv_bytes = (8 + idx) * nnz + 8 * (rows + 1) + 16 * rows
+    asm_bytes = (8 + idx) * nnz + 8 * (rows + 1)
+    del m
+    return {"config": f"5: 73-pt clamped CSR 255^3 (int{bits} cols)", "rows": rows, "nnz": nnz,
+            "assembly_ms": asm_ms, "assembly_gbs_written": asm_bytes / (asm_ms * 1e-3) / 1e9,
+            "spmv_ms": ms, "spmv_grows_per_s": rows / (ms * 1e-3) / 1e9,
+            "spmv_achieved_gbs": spmv_bytes / (ms * 1e-3) / 1e9}
+
+
+def extra_cg(lib, N: int = 1024, iters: int = 256):
+    """Config 2 at N=1024: time a fixed number of device CG iterations (13-pt clamped)."""
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.errors import StencilkitError
+    from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, assemble, make_grid
+    from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve
+    from paper_2205_03354_b200.stencil import bilaplacian
+
+    g = make_grid(2, N + 1, 1.0 / N, BoundaryKind.clamped)
+    m = assemble(DeviceStencil(bilaplacian(2)), g)
+    b = DeviceArray.from_host(field(3, m.rows, 1.0))
+    x = DeviceArray(m.rows)
+    opts = SolveOptions(rel_tol=1e-30, max_iter=iters, check_every=64)
+    for _ in range(1):
+        try:
+            cg_solve(m, b, opts, x_out=x)
+        except StencilkitError:
+            pass
+    ev = Events(lib)
+    rep = SolveReport()
+    ev.start()
+    try:
+        cg_solve(m, b, opts, rep, x_out=x)
+    except StencilkitError:
+        pass
+    ms = ev.stop_ms()
+    per = ms / max(rep.iterations, 1)
+    bytes_it = 16 * m.nnz() + 8 * (m.rows + 1) + 16 * m.rows + 48 * m.rows + 24 * m.rows
+    return {"config": f"2: CG 13-pt clamped N={N} ({m.rows} rows)", "iterations": rep.iterations,
+            "ms_per_iteration": per, "achieved_gbs": bytes_it / (per * 1e-3) / 1e9}
+
+
+# ----------------------------------------------------------- CPU reference --
+def ref_ch_steps_per_s(dim: int, steps: int, warmup: int):
+    """The reference library on the host cores: restated explicit CH step."""
+    from oracle.ffi import Reference
+
+    n, h, p, dt, seed = ch_setup(dim)
+    ref = Reference()
+    t0 = time.perf_counter()
+    handle = ref.ch_create(dim, n, h, p)
+    setup_s = time.perf_counter() - t0
+    c = ref.uniform(seed, n ** dim) * 0.05
+    ref.ch_steps(handle, dt, warmup, c)
+    t0 = time.perf_counter()
+    ref.ch_steps(handle, dt, steps, c)
+    el = time.perf_counter() - t0
+    ref.ch_free(handle)
+    return steps / el, el, setup_s, ref.threads()
+
+
+# ------------------------------------------------------------------- main --
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["ch3d", "ch2d"], default="ch3d")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=10, help="CPU-baseline sample (steps)")
+    args = ap.parse_args()
+    dim = 3 if args.workload == "ch3d" else 2
+    n, h, p, dt, seed = ch_setup(dim)
+    workload = (f"config {4 if dim == 3 else 3}: fused explicit Cahn-Hilliard step, periodic fp64 {n}^{dim}, "
+                f"eps={0.02 if dim == 3 else 0.01}, dt={dt:.4e}, composed {25 if dim == 3 else 13}-pt B + "
+                f"{7 if dim == 3 else 5}-pt L on f'(u)")
+    config = {"workload": workload, "grid": [n] * dim, "points_per_step": n ** dim, "dtype": "fp64",
+              "l2": "inputs larger than L2 (2 x 134 MB fields)" if dim == 3 else
+              "2 x 33.5 MB fields fit in the 126 MB L2", "parallelism": f"replicas x{args.gpus}"}
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return 0
+        sps, el, setup_s, threads = ref_ch_steps_per_s(dim, args.steps, args.warmup)
+        line = {"metric": "CH steps/s", "value": sps, "unit": "steps/s", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 / sps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded mt19937_64 uniform noise, as the configs specify)",
+                "config": config,
+                "cpu_baseline": {"value": sps, "unit": "steps/s", "cores": threads, "kind": "reference",
+                                 "sample": f"{args.steps} timed steps after {args.warmup} warm-up on the full "
+                                           f"{n}^{dim} grid (L, B assembly {setup_s:.1f}s excluded)"},
+                "e2e": {"value": sps, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    d = Dist()
+    from paper_2205_03354_b200 import _lib
+
+    lib = _lib.ensure_device(d.local)
+    r = run_ch(lib, dim, args.steps, args.warmup, d)
+    ms_step = r["ms"] / args.steps
+    steps_per_s = args.steps / (r["ms"] * 1e-3)
+    value = steps_per_s * d.world  # whole job: replicas
+    peak, peak_kind = peak_hbm()
+    bytes_step = 16.0 * r["points"]
+    achieved = bytes_step / (ms_step * 1e-3) / 1e9
+    kernel = "stencil3d_kernel<CahnHilliard>" if dim == 3 else "stencil2d_kernel<CahnHilliard>"
+    line = {
+        "metric": "CH steps/s",
+        "value": value,
+        "unit": "steps/s",
+        "n_gpus": d.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded mt19937_64 uniform noise, as the configs specify)",
+        "config": config,
+        "gpoints_per_s": r["points"] / (ms_step * 1e-3) / 1e9 * d.world,
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy read+write)", "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(kernel),
+                     "algorithmic_bytes_per_launch": bytes_step},
+    }
+    if "e2e_s" in r:
+        line["e2e"] = {"value": args.steps / r["e2e_s"] * d.world, "unit": "steps/s",
+                       "h2d_bytes_per_step": r["e2e_bytes"] / args.steps,
+                       "d2h_bytes_per_step": r["e2e_bytes"] / args.steps,
+                       "note": f"sk_ch_explicit_host: one H2D of the {r['e2e_bytes']} B field (pinned), "
+                               f"{args.steps} steps, one D2H; bytes per step amortised"}
+    if d.rank == 0 and not args.no_extra and d.world == 1:
+        extra = []
+        for fn in (lambda: extra_apply2d(lib), lambda: run_ch_2d_extra(lib, dim, args),
+                   lambda: extra_apply3d(lib, "25"), lambda: extra_apply3d(lib, "73"),
+                   lambda: extra_csr73(lib, 64), lambda: extra_csr73(lib, 32), lambda: extra_cg(lib)):
+            try:
+                e = fn()
+                if e:
+                    if "achieved_gbs" in e:
+                        e["frac_of_peak"] = e["achieved_gbs"] / peak
+                    if "spmv_achieved_gbs" in e:
+                        e["spmv_frac_of_peak"] = e["spmv_achieved_gbs"] / peak
+                    extra.append(e)
+            except Exception as ex:  # keep the headline line even if an extra fails
+                extra.append({"error": repr(ex)})
+        line["extra"] = extra
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+        try:
+            sps, el, setup_s, threads = ref_ch_steps_per_s(dim, args.cpu_steps, 1)
+            line["cpu_baseline"] = {"value": sps, "unit": "steps/s", "cores": threads, "kind": "reference",
+                                    "sample": f"{args.cpu_steps} steps of the full {n}^{dim} grid "
+                                              f"({el:.1f}s; L,B assembly {setup_s:.1f}s excluded)"}
+        except Exception as ex:
+            line["cpu_baseline"] = {"error": repr(ex)}
+    if d.rank == 0:
+        print(json.dumps(line))
+    d.close()
+    return 0
+
+
+def run_ch_2d_extra(lib, dim, args):
+    """The other CH config (config 3 when the headline is config 4)."""
+    other = 2 if dim == 3 else 3
+    r = run_ch(lib, other, 200, 5, _NoDist(), e2e=False)
+    ms = r["ms"] / 200
+    return {"config": f"{3 if other == 2 else 4}: CH {r['n']}^{other}", "value": 1e3 / ms, "unit": "steps/s",
+            "ms_per_step": ms, "achieved_gbs": 16.0 * r["points"] / (ms * 1e-3) / 1e9,
+            "note": "2 x 33.5 MB fields stay L2-resident" if other == 2 else ""}
+
+
+class _NoDist:
+    world, rank, local = 1, 0, 0
+
+    def barrier(self):
+        pass
+
+    def max(self, x):
+        return x
+
+
+if __name__ == "__main__":
+    sys.exit(main())

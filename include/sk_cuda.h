@@ -119,6 +119,16 @@ int sk_stream_sync(void* stream);
 int sk_fill_uniform_host(uint64_t seed, int64_t count, double lo, double hi, double* out);
 /* Number of kernel launches this library has issued (monotone counter). */
 int64_t sk_launch_count(void);
+/* Page-lock a caller host buffer so *_host calls copy at full PCIe/C2C rate. */
+int sk_host_register(void* host_ptr, size_t bytes);
+int sk_host_unregister(void* host_ptr);
+/* CUDA events for device-side timing on the launching stream. */
+int sk_event_create(void** ev);
+int sk_event_destroy(void* ev);
+int sk_event_record(void* ev, void* stream);
+int sk_event_elapsed_ms(void* start, void* end, float* ms); /* waits for `end` */
+/* Evict L2 by writing a buffer larger than it (timing hygiene). */
+int sk_l2_flush(void* stream);
 
 /* ---- stencil (host composition result -> device) ------------------------
  * Replaces handing a `stencilkit::Stencil` (stencil.hpp:19-42) to assemble().

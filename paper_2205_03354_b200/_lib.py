@@ -51,6 +51,13 @@ SIGNATURES = {
     "sk_stream_sync": (c_int, [vp]),
     "sk_fill_uniform_host": (c_int, [C.c_uint64, c_i64, c_dbl, c_dbl, vp]),
     "sk_launch_count": (c_i64, []),
+    "sk_host_register": (c_int, [vp, C.c_size_t]),
+    "sk_host_unregister": (c_int, [vp]),
+    "sk_event_create": (c_int, [C.POINTER(vp)]),
+    "sk_event_destroy": (c_int, [vp]),
+    "sk_event_record": (c_int, [vp, vp]),
+    "sk_event_elapsed_ms": (c_int, [vp, vp, C.POINTER(C.c_float)]),
+    "sk_l2_flush": (c_int, [vp]),
     "sk_stencil_create": (c_int, [c_int, c_int, vp, vp, c_int, C.POINTER(vp)]),
     "sk_stencil_destroy": (c_int, [vp]),
     "sk_stencil_kernel_class": (c_int, [vp]),

@@ -371,21 +371,19 @@ int sk_cg_solve_host(const sk_csr* m, const double* b_host, double* x_host, cons
   if (!m) return fail(SK_ERR_INVALID_ARGUMENT, "null matrix");
   if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
   if (m->rows == 0) return SK_OK;
-  const size_t bytes = sizeof(double) * size_t(m->rows);
-  double *b = nullptr, *x = nullptr;
-  SK_CUDA_TRY(cudaMalloc(&b, bytes));
-  cudaError_t e = cudaMalloc(&x, bytes);
-  int st = e == cudaSuccess ? SK_OK : cuda_fail(e, "cudaMalloc");
-  if (st == SK_OK && (e = cudaMemcpy(b, b_host, bytes, cudaMemcpyHostToDevice)) != cudaSuccess) st = cuda_fail(e, "H2D");
-  if (st == SK_OK) st = cg_solve(m, b, x, o, rep, nullptr);
   // the last iterate is returned even on NoConvergence
-  if ((st == SK_OK || st == SK_ERR_NO_CONVERGENCE)) {
-    cudaError_t e2 = cudaMemcpy(x_host, x, bytes, cudaMemcpyDeviceToHost);
-    if (e2 != cudaSuccess && st == SK_OK) st = cuda_fail(e2, "D2H");
-  }
-  cudaFree(b);
-  if (x) cudaFree(x);
-  return st;
+  int solve_status = SK_OK;
+  std::string msg;
+  int st = host_roundtrip(b_host, size_t(m->rows), x_host, size_t(m->rows),
+                          [&](const double* b, double* x, cudaStream_t s) {
+                            solve_status = cg_solve(m, b, x, o, rep, s);
+                            if (solve_status != SK_OK && solve_status != SK_ERR_NO_CONVERGENCE) return solve_status;
+                            if (solve_status != SK_OK) msg = sk_last_error();
+                            return int(SK_OK);
+                          });
+  if (st != SK_OK) return st;
+  if (solve_status != SK_OK) return fail(solve_status, msg.substr(msg.find(": ") + 2));
+  return SK_OK;
 }
 
 }  // extern "C"

@@ -17,14 +17,15 @@
 
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
+#include "sk_stream3d.cuh"
 
 namespace sk {
 
 template <Mode M>
 int launch_2d(const Apply2DArgs& a, cudaStream_t stream);
 template <Mode M, class C>
-int launch_3d(Apply3DArgs a, cudaStream_t stream);
-using C3R2 = Cfg3D<2, 64, 16, 2, 2, 4>;
+int launch_3d(Args3D a, cudaStream_t stream);
+using C3R2 = Cfg3CH;
 
 namespace {
 
@@ -108,7 +109,9 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   OrbitW wb{};
   for (int i = 0; i < 8; ++i) wb.w[i] = (bilap->orbit_coeff[i] * sb) * fac_b;
   const double wl0 = (lap->orbit_coeff[0] * sl) * dtm, wl1 = (lap->orbit_coeff[1] * sl) * dtm;
-  const ChemParams chem{p->rho_w, p->c_alpha, p->c_beta};
+  // f'(c) = 2 rho (c-a)(c-b)(2c-a-b) as a cubic (cahn_hilliard.cpp:70-73 expanded)
+  const double ca = p->c_alpha, cb = p->c_beta, s = ca + cb, pr = ca * cb, r2 = 2.0 * p->rho_w;
+  const Poly3 chem{2.0 * r2, -3.0 * r2 * s, r2 * (s * s + 2.0 * pr), -r2 * pr * s};
   if (g.dim == 2) {
     Apply2DArgs a{};
     a.u = in;
@@ -119,20 +122,20 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
     a.wl0 = wl0;
     a.wl1 = wl1;
     a.chem = chem;
-    a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= 64 + 4;
+    a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= 64 + 4 && a.ny >= 32 + 4;
     return launch_2d<Mode::CahnHilliard>(a, stream);
   }
-  Apply3DArgs a{};
+  Args3D a{};
   a.u = in;
   a.v = out;
   a.nx = g.n[0];
   a.ny = g.n[1];
   a.nz = g.n[2];
-  a.w = wb;
+  for (int i = 0; i < 8; ++i) a.w[i] = wb.w[i];
   a.wl0 = wl0;
   a.wl1 = wl1;
   a.chem = chem;
-  a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R;
+  a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R;
   return launch_3d<Mode::CahnHilliard, C3R2>(a, stream);
 }
 
@@ -243,20 +246,18 @@ int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk
   GridInfo g;
   if (int st = grid_info(gd, &g)) return st;
   if (!c_host && g.rows > 0) return fail(SK_ERR_INVALID_ARGUMENT, "null host field");
-  const size_t bytes = sizeof(double) * size_t(g.rows);
-  double *c = nullptr, *s = nullptr;
-  SK_CUDA_TRY(cudaMalloc(&c, bytes));
-  cudaError_t e = cudaMalloc(&s, bytes);
-  int st = e == cudaSuccess ? SK_OK : cuda_fail(e, "cudaMalloc");
-  if (st == SK_OK && (e = cudaMemcpy(c, c_host, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
-    st = cuda_fail(e, "H2D");
-  int in_scratch = 0;
-  if (st == SK_OK) st = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, c, s, &in_scratch, nullptr);
-  if (st == SK_OK && (e = cudaMemcpy(c_host, in_scratch ? s : c, bytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
-    st = cuda_fail(e, "D2H");
-  cudaFree(c);
-  if (s) cudaFree(s);
-  return st;
+  // c_host -> c (device), steps ping-pong c <-> s, result -> c_host
+  cudaStream_t hs = host_stream();
+  AsyncBuf s(hs);
+  SK_CUDA_TRY(s.alloc(sizeof(double) * size_t(g.rows)));
+  return host_roundtrip(c_host, size_t(g.rows), nullptr, 0, [&](const double* c, double*, cudaStream_t st) {
+    int in_scratch = 0;
+    double* cd = const_cast<double*>(c);
+    if (int e = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, cd, s.d(), &in_scratch, st)) return e;
+    SK_CUDA_TRY(cudaMemcpyAsync(c_host, in_scratch ? s.d() : cd, sizeof(double) * size_t(g.rows),
+                                cudaMemcpyDeviceToHost, st));
+    return int(SK_OK);
+  });
 }
 
 int sk_free_energy(const sk_grid_desc* gd, const sk_ch_params* p, const double* c, double* energy, void* stream_p) {

@@ -113,6 +113,11 @@ int sk_device_init(int device) {
   if (device < 0 || device >= count) return fail(SK_ERR_NO_DEVICE, "device ordinal out of range");
   SK_CUDA_TRY(cudaSetDevice(device));
   SK_CUDA_TRY(cudaFree(nullptr));
+  // keep stream-ordered scratch in the pool between calls (no OS round trips)
+  cudaMemPool_t pool;
+  SK_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = UINT64_MAX;
+  SK_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   return SK_OK;
 }
 
@@ -144,6 +149,49 @@ int sk_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
 
 int sk_stream_sync(void* stream) {
   SK_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  return SK_OK;
+}
+
+int sk_host_register(void* p, size_t bytes) {
+  if (!p || bytes == 0) return fail(SK_ERR_INVALID_ARGUMENT, "bad host buffer");
+  SK_CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return SK_OK;
+}
+
+int sk_host_unregister(void* p) {
+  SK_CUDA_TRY(cudaHostUnregister(p));
+  return SK_OK;
+}
+
+int sk_event_create(void** ev) {
+  if (!ev) return fail(SK_ERR_INVALID_ARGUMENT, "null event");
+  cudaEvent_t e;
+  SK_CUDA_TRY(cudaEventCreate(&e));
+  *ev = e;
+  return SK_OK;
+}
+
+int sk_event_destroy(void* ev) {
+  if (ev) SK_CUDA_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+  return SK_OK;
+}
+
+int sk_event_record(void* ev, void* stream) {
+  SK_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev), as_stream(stream)));
+  return SK_OK;
+}
+
+int sk_event_elapsed_ms(void* a, void* b, float* ms) {
+  SK_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(b)));
+  SK_CUDA_TRY(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
+  return SK_OK;
+}
+
+int sk_l2_flush(void* stream) {
+  static void* buf = nullptr;
+  const size_t bytes = size_t(512) << 20;  // 512 MiB > 126 MB L2
+  if (!buf) SK_CUDA_TRY(cudaMalloc(&buf, bytes));
+  SK_CUDA_TRY(cudaMemsetAsync(buf, 0, bytes, as_stream(stream)));
   return SK_OK;
 }
 

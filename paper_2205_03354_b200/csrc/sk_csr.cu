@@ -499,18 +499,8 @@ int sk_csr_matvec(const sk_csr* m, const double* x, double* y, void* stream) {
 int sk_csr_matvec_host(const sk_csr* m, const double* x_host, double* y_host) {
   if (!m) return fail(SK_ERR_INVALID_ARGUMENT, "null matrix");
   if (m->rows == 0) return SK_OK;
-  double *x = nullptr, *y = nullptr;
-  SK_CUDA_TRY(cudaMalloc(&x, sizeof(double) * size_t(m->cols)));
-  cudaError_t e = cudaMalloc(&y, sizeof(double) * size_t(m->rows));
-  int st = e == cudaSuccess ? SK_OK : cuda_fail(e, "cudaMalloc");
-  if (st == SK_OK && (e = cudaMemcpy(x, x_host, sizeof(double) * size_t(m->cols), cudaMemcpyHostToDevice)) != cudaSuccess)
-    st = cuda_fail(e, "H2D");
-  if (st == SK_OK) st = csr_spmv(m, x, y, nullptr);
-  if (st == SK_OK && (e = cudaMemcpy(y_host, y, sizeof(double) * size_t(m->rows), cudaMemcpyDeviceToHost)) != cudaSuccess)
-    st = cuda_fail(e, "D2H");
-  cudaFree(x);
-  if (y) cudaFree(y);
-  return st;
+  return host_roundtrip(x_host, size_t(m->cols), y_host, size_t(m->rows),
+                        [&](const double* x, double* y, cudaStream_t st) { return csr_spmv(m, x, y, st); });
 }
 
 }  // extern "C"

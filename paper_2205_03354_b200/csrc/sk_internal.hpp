@@ -48,7 +48,36 @@ int check_width(const sk_stencil* s, const GridInfo& g);
 // Launch one matrix-free application on `stream` (device pointers).
 int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream);
 
-// Internal stream for graph capture when the caller passes the legacy stream.
+// Internal per-thread non-blocking stream: graph capture when the caller
+// passes the legacy stream, and the stream every *_host entry point runs on.
 cudaStream_t capture_stream();
+inline cudaStream_t host_stream() { return capture_stream(); }
+
+// Stream-ordered scratch for *_host calls (pool allocator: no cudaMalloc
+// synchronisation inside a timed end-to-end call).
+struct AsyncBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  explicit AsyncBuf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 16, s); }
+  double* d() const { return static_cast<double*>(p); }
+  ~AsyncBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+// Copy host -> device, run `body` on the host stream, copy device -> host, sync.
+template <class Body>
+int host_roundtrip(const double* in_host, size_t in_count, double* out_host, size_t out_count, Body body) {
+  cudaStream_t s = host_stream();
+  AsyncBuf in(s), out(s);
+  SK_CUDA_TRY(in.alloc(in_count * sizeof(double)));
+  SK_CUDA_TRY(out.alloc(out_count * sizeof(double)));
+  if (in_count) SK_CUDA_TRY(cudaMemcpyAsync(in.p, in_host, in_count * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (int st = body(in.d(), out.d(), s)) return st;
+  if (out_count) SK_CUDA_TRY(cudaMemcpyAsync(out_host, out.p, out_count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SK_CUDA_TRY(cudaStreamSynchronize(s));
+  return SK_OK;
+}
 
 }  // namespace sk

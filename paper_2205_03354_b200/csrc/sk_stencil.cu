@@ -16,6 +16,7 @@
 
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
+#include "sk_stream3d.cuh"
 
 sk_stencil::~sk_stencil() {
   if (rep_exec) cudaGraphExecDestroy(rep_exec);
@@ -125,9 +126,17 @@ int check_width(const sk_stencil* s, const GridInfo& g) {
 
 // ---- kernel configurations ----------------------------------------------
 using T2 = Tile2D<64, 32, 2, 4>;
-using C3R2 = Cfg3D<2, 64, 16, 2, 2, 4>;
-using C3R4 = Cfg3D<4, 64, 16, 2, 2, 4>;
-constexpr int kChunkZ = 32;
+using C3R2 = Cfg3R2;
+using C3R4 = Cfg3R4;
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = kNumSMs;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
 
 template <Mode M>
 int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
@@ -141,21 +150,33 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
 }
 
 template <Mode M, class C>
-int launch_3d(Apply3DArgs a, cudaStream_t stream) {
-  auto kern = stencil3d_kernel<M, C>;
+int launch_3d(Args3D a, cudaStream_t stream) {
+  auto kern = stream3d_kernel<M, C>;
   static int once = set_smem(kern, C::SMEM_BYTES);
   if (once != SK_OK) return once;
   a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
-  const int tiles_y = int((a.ny + C::TY - 1) / C::TY);
-  a.cz = kChunkZ;
-  dim3 grid(unsigned(a.tiles_x * tiles_y), unsigned((a.nz + a.cz - 1) / a.cz));
-  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(a);
-  SK_LAUNCH_CHECK("stencil3d_kernel");
+  a.tiles_y = int((a.ny + C::TY - 1) / C::TY);
+  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
+  // persistent: MIN_BLOCKS CTAs per SM, each a balanced contiguous unit range
+  int64_t grid = int64_t(num_sms()) * C::MIN_BLOCKS;
+  if (grid > units) grid = units;
+  // z-chunk: the smallest divisor of nz covering one CTA's share, so CTAs
+  // start together at the chunk tops and neighbouring tiles advance in step
+  const int64_t share = (units + grid - 1) / grid;
+  a.zchunk = a.nz;
+  for (int64_t d = 1; d <= a.nz; ++d)
+    if (a.nz % d == 0 && d >= share) {
+      a.zchunk = d;
+      break;
+    }
+  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;  // int32 in-plane offsets
+  kern<<<unsigned(grid), C::THREADS, C::SMEM_BYTES, stream>>>(a);
+  SK_LAUNCH_CHECK("stream3d_kernel");
   return SK_OK;
 }
 
 template int launch_2d<Mode::CahnHilliard>(const Apply2DArgs&, cudaStream_t);
-template int launch_3d<Mode::CahnHilliard, C3R2>(Apply3DArgs, cudaStream_t);
+template int launch_3d<Mode::CahnHilliard, Cfg3CH>(Args3D, cudaStream_t);
 
 int launch_generic(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream) {
   GenericArgs a{};
@@ -198,22 +219,24 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     a.nx = g.n[0];
     a.ny = g.n[1];
     a.w = w;
-    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= 64 + 4 && aligned16(u) && aligned16(v);
+    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= 64 + 4 && a.ny >= 32 + 4 && aligned16(u) && aligned16(v);
     return launch_2d<Mode::Apply>(a, stream);
   }
   if ((s->kclass == 2 || s->kclass == 3) && g.dim == 3 && all_periodic(g)) {
-    Apply3DArgs a{};
+    Args3D a{};
     a.u = u;
     a.v = v;
     a.nx = g.n[0];
     a.ny = g.n[1];
     a.nz = g.n[2];
-    a.w = w;
+    for (int i = 0; i < 8; ++i) a.w[i] = w.w[i];
     if (s->kclass == 2) {
-      a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && aligned16(u) && aligned16(v);
+      a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R &&
+                  aligned16(u) && aligned16(v);
       return launch_3d<Mode::Apply, C3R2>(a, stream);
     }
-    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && aligned16(u) && aligned16(v);
+    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
+                aligned16(u) && aligned16(v);
     return launch_3d<Mode::Apply, C3R4>(a, stream);
   }
   return launch_generic(s, g, u, v, stream);
@@ -346,20 +369,8 @@ int sk_composed_apply_host(const sk_stencil* s, const sk_grid_desc* gd, const do
   if (int st = check_width(s, g)) return st;
   if (g.rows == 0) return SK_OK;
   if (!u_host || !v_host) return fail(SK_ERR_INVALID_ARGUMENT, "null host buffer");
-  const size_t bytes = sizeof(double) * size_t(g.rows);
-  double *du = nullptr, *dv = nullptr;
-  SK_CUDA_TRY(cudaMalloc(&du, bytes));
-  cudaError_t e = cudaMalloc(&dv, bytes);
-  int st = SK_OK;
-  if (e != cudaSuccess) st = cuda_fail(e, "cudaMalloc");
-  if (st == SK_OK && (e = cudaMemcpy(du, u_host, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
-    st = cuda_fail(e, "H2D");
-  if (st == SK_OK) st = launch_apply(s, g, du, dv, nullptr);
-  if (st == SK_OK && (e = cudaMemcpy(v_host, dv, bytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
-    st = cuda_fail(e, "D2H");
-  cudaFree(du);
-  if (dv) cudaFree(dv);
-  return st;
+  return host_roundtrip(u_host, size_t(g.rows), v_host, size_t(g.rows),
+                        [&](const double* du, double* dv, cudaStream_t st) { return launch_apply(s, g, du, dv, st); });
 }
 
 }  // extern "C"

@@ -50,6 +50,17 @@ __device__ __forceinline__ double chem_prime(double c, const ChemParams& p) {
   return __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, p.rho_w), a), b), t);
 }
 
+// f'(c) expanded on the host into a cubic, evaluated with 3 FMAs:
+//   2 rho (c-a)(c-b)(2c-a-b) = 4rho c^3 - 6rho(a+b) c^2 + 2rho((a+b)^2 + 2ab) c - 2rho ab(a+b)
+// (for rho = 1/4, a = -1, b = 1 exactly c^3 - c).
+struct Poly3 {
+  double k3, k2, k1, k0;
+};
+
+__device__ __forceinline__ double poly3(double c, const Poly3& p) {
+  return fma(fma(fma(p.k3, c, p.k2), c, p.k1), c, p.k0);
+}
+
 enum class Mode { Apply = 0, CahnHilliard = 1 };
 
 // Apply outputs are never re-read by the next launch (config 1 ping-pongs
@@ -84,7 +95,7 @@ struct Apply2DArgs {
   int64_t nx, ny;
   OrbitW w;      // scaled orbit weights of the composed stencil (Apply) or B' (CH)
   double wl0, wl1;  // CH: scaled 5-point Laplacian weights (center, axis)
-  ChemParams chem;
+  Poly3 chem;
   int bulk_ok;   // 1: nx even and >= TX+4 -> TMA bulk row copies
 };
 
@@ -94,29 +105,17 @@ __device__ __forceinline__ void load_tile_2d(double* tile, uint64_t* bar, const 
   using T = Tile2D<TX, TY, PX, PY>;
   constexpr int R = T::R;
   const int tid = threadIdx.x;
+  (void)bar;
   if (a.bulk_ok) {
-    if (tid < 32) {
-      if (tid == 0) mbar_arrive_expect_tx(bar, T::ROWS * T::PITCH * 8);
-      __syncwarp();
-      const int64_t xs = x0 - R;  // may be -R or run past nx: split into <= 2 pieces
-      for (int r = tid; r < T::ROWS; r += 32) {
-        int64_t gy = y0 - R + r;
-        gy = wrap_idx(gy, a.ny);
-        const double* row = a.u + gy * a.nx;
-        double* dst = tile + r * T::PITCH;
-        if (xs < 0) {
-          bulk_g2s(dst, row + (a.nx + xs), uint32_t(-xs) * 8, bar);
-          bulk_g2s(dst - xs, row, uint32_t(T::PITCH + xs) * 8, bar);
-        } else if (xs + T::PITCH > a.nx) {
-          const uint32_t first = uint32_t(a.nx - xs);
-          bulk_g2s(dst, row + xs, first * 8, bar);
-          bulk_g2s(dst + first, row, uint32_t(T::PITCH - first) * 8, bar);
-        } else {
-          bulk_g2s(dst, row + xs, T::PITCH * 8, bar);
-        }
-      }
+    // every thread issues 16-byte cp.async (LDGSTS) pairs of the haloed tile
+    constexpr int HP = T::PITCH / 2;
+    for (int i = tid; i < T::ROWS * HP; i += T::THREADS) {
+      const int r = i / HP, c = 2 * (i - r * HP);
+      const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
+      cp_async16(tile + r * T::PITCH + c, a.u + gy * a.nx + gx);
     }
-    mbar_wait(bar, 0);
+    cp_async_wait_all();
+    __syncthreads();
   } else {
     for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {
       const int r = i / T::PITCH, c = i % T::PITCH;
@@ -186,9 +185,9 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
         // L f'(c): 5-point on g = f'(c); g at this row's point (for |d| = 1)
         // and the row neighbours (for d = 0). Vertical neighbours arrive as
         // the g-centre of adjacent rows through the |d| = 1 slice.
-        const double g = chem_prime(c, a.chem);
+        const double g = poly3(c, a.chem);
         if (need0) {
-          const double gp = chem_prime(u[i + R - 1], a.chem) + chem_prime(u[i + R + 1], a.chem);
+          const double gp = poly3(u[i + R - 1], a.chem) + poly3(u[i + R + 1], a.chem);
           s0 = fma(a.wl1, gp, fma(a.wl0, g, s0));
         }
         if (need1) s1 = fma(a.wl1, g, s1);
@@ -222,244 +221,6 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
 #pragma unroll
       for (int i = 0; i < PX; ++i)
         if (gx + i < a.nx) out[i] = val[i];
-    }
-  }
-}
-
-// =========================================================================
-// 3D: warp-specialised streaming along z. CTA = TX x TY column of the grid
-// over a chunk of CZ output planes; ring of STAGES plane buffers
-// ((TY+2R) x (TX+2R) doubles each) filled by one producer warp with TMA bulk
-// row copies; 8 consumer warps, each thread PX x PY points, register queue of
-// 2R+1 output planes rotated by loop unrolling (no register moves).
-// =========================================================================
-template <int R_, int TX_, int TY_, int PX_, int PY_, int STAGES_>
-struct Cfg3D {
-  static constexpr int R = R_, TX = TX_, TY = TY_, PX = PX_, PY = PY_, STAGES = STAGES_;
-  static constexpr int PITCH = TX + 2 * R;
-  static constexpr int ROWS = TY + 2 * R;
-  static constexpr int PLANE = ROWS * PITCH;  // doubles
-  static constexpr int CONSUMERS = (TX / PX) * (TY / PY);
-  static_assert(CONSUMERS % 32 == 0, "consumer threads must be whole warps");
-  static constexpr int CONSUMER_WARPS = CONSUMERS / 32;
-  static constexpr int THREADS = CONSUMERS + 32;
-  static constexpr int BAR_BYTES = 2 * STAGES * 8;
-  static constexpr int SMEM_BYTES = 128 + STAGES * PLANE * 8;
-  static constexpr int Q = 2 * R + 1;
-};
-
-struct Apply3DArgs {
-  const double* __restrict__ u;
-  double* __restrict__ v;
-  int64_t nx, ny, nz;
-  int cz;        // output planes per CTA
-  int tiles_x;   // CTAs along x
-  OrbitW w;
-  double wl0, wl1;
-  ChemParams chem;
-  int bulk_ok;
-};
-
-template <class C>
-__device__ __forceinline__ void produce_plane_3d(double* buf, uint64_t* full, const Apply3DArgs& a, int64_t x0,
-                                                 int64_t y0, int64_t gz, int lane) {
-  constexpr int R = C::R;
-  const double* plane = a.u + gz * a.nx * a.ny;
-  if (a.bulk_ok) {
-    if (lane == 0) mbar_arrive_expect_tx(full, C::PLANE * 8);
-    __syncwarp();
-    const int64_t xs = x0 - R;
-    for (int r = lane; r < C::ROWS; r += 32) {
-      const int64_t gy = wrap_idx(y0 - R + r, a.ny);
-      const double* row = plane + gy * a.nx;
-      double* dst = buf + r * C::PITCH;
-      if (xs < 0) {
-        bulk_g2s(dst, row + (a.nx + xs), uint32_t(-xs) * 8, full);
-        bulk_g2s(dst - xs, row, uint32_t(C::PITCH + xs) * 8, full);
-      } else if (xs + C::PITCH > a.nx) {
-        const uint32_t first = uint32_t(a.nx - xs);
-        bulk_g2s(dst, row + xs, first * 8, full);
-        bulk_g2s(dst + first, row, uint32_t(C::PITCH - first) * 8, full);
-      } else {
-        bulk_g2s(dst, row + xs, C::PITCH * 8, full);
-      }
-    }
-  } else {
-    for (int i = lane; i < C::PLANE; i += 32) {
-      const int r = i / C::PITCH, c = i % C::PITCH;
-      const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
-      buf[i] = __ldg(plane + gy * a.nx + gx);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(full);
-  }
-}
-
-// In-plane orbit sums at tile position (ly, lx) for the point set of one
-// thread. Slices per radius:
-//   R=2 (25-pt): S0 = w0 c + w1 A1 + w2 D11 + w3 A2 ; S1 = w1 c + w2 A1 ; S2 = w3 c
-//   R=4 (73-pt): S0 = w0 c + w1 A1 + w2 D11 + w3 A2 + w4 D21 + w5 D22 + w6 A3 + w7 A4
-//                S1 = w1 c + w2 A1 + w4 A2 ; S2 = w3 c + w4 A1 + w5 A2 ; S3 = w6 c ; S4 = w7 c
-template <int R>
-__device__ __forceinline__ void slices_3d(const double* __restrict__ buf, int pitch, int ly, int lx, const OrbitW& w,
-                                          double* s) {
-  auto at = [&](int dy, int dx) { return buf[(ly + dy) * pitch + lx + dx]; };
-  const double c = at(0, 0);
-  const double a1 = (at(0, -1) + at(0, 1)) + (at(-1, 0) + at(1, 0));
-  if constexpr (R == 2) {
-    const double d11 = (at(-1, -1) + at(-1, 1)) + (at(1, -1) + at(1, 1));
-    const double a2 = (at(0, -2) + at(0, 2)) + (at(-2, 0) + at(2, 0));
-    s[0] = fma(w.w[3], a2, fma(w.w[2], d11, fma(w.w[1], a1, w.w[0] * c)));
-    s[1] = fma(w.w[2], a1, w.w[1] * c);
-    s[2] = w.w[3] * c;
-  } else {
-    const double d11 = (at(-1, -1) + at(-1, 1)) + (at(1, -1) + at(1, 1));
-    const double a2 = (at(0, -2) + at(0, 2)) + (at(-2, 0) + at(2, 0));
-    const double d21 = ((at(-1, -2) + at(-1, 2)) + (at(1, -2) + at(1, 2))) +
-                       ((at(-2, -1) + at(-2, 1)) + (at(2, -1) + at(2, 1)));
-    const double d22 = (at(-2, -2) + at(-2, 2)) + (at(2, -2) + at(2, 2));
-    const double a3 = (at(0, -3) + at(0, 3)) + (at(-3, 0) + at(3, 0));
-    const double a4 = (at(0, -4) + at(0, 4)) + (at(-4, 0) + at(4, 0));
-    s[0] = fma(w.w[7], a4,
-               fma(w.w[6], a3,
-                   fma(w.w[5], d22, fma(w.w[4], d21, fma(w.w[3], a2, fma(w.w[2], d11, fma(w.w[1], a1, w.w[0] * c)))))));
-    s[1] = fma(w.w[4], a2, fma(w.w[2], a1, w.w[1] * c));
-    s[2] = fma(w.w[5], a2, fma(w.w[4], a1, w.w[3] * c));
-    s[3] = w.w[6] * c;
-    s[4] = w.w[7] * c;
-  }
-}
-
-template <Mode M, class C>
-__global__ void __launch_bounds__(C::THREADS) stencil3d_kernel(const Apply3DArgs a) {
-  constexpr int R = C::R, Q = C::Q, S = C::STAGES;
-  constexpr int NPT = C::PX * C::PY;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* empty = full + S;
-  double* ring = reinterpret_cast<double*>(smem_raw + 128);
-
-  const int tile = blockIdx.x;
-  const int64_t x0 = int64_t(tile % a.tiles_x) * C::TX;
-  const int64_t y0 = int64_t(tile / a.tiles_x) * C::TY;
-  const int64_t z0 = int64_t(blockIdx.y) * a.cz;
-  const int cz = int(a.nz - z0 < int64_t(a.cz) ? a.nz - z0 : int64_t(a.cz));
-  const int np = cz + 2 * R;  // input planes z0-R .. z0+cz-1+R
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::CONSUMER_WARPS);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == C::CONSUMER_WARPS) {  // ---- producer warp ----
-    for (int p = 0; p < np; ++p) {
-      const int s = p % S;
-      if (p >= S) mbar_wait(&empty[s], ((p / S) - 1) & 1);
-      const int64_t gz = wrap_idx(z0 - R + p, a.nz);
-      produce_plane_3d<C>(ring + s * C::PLANE, &full[s], a, x0, y0, gz, lane);
-    }
-    return;
-  }
-
-  // ---- consumer warps ----
-  const int tx = threadIdx.x % (C::TX / C::PX), ty = threadIdx.x / (C::TX / C::PX);
-  const int lx0 = tx * C::PX + R, ly0 = ty * C::PY + R;
-  const int64_t gx0 = x0 + tx * C::PX;
-
-  double q[Q][NPT];
-#pragma unroll
-  for (int t = 0; t < Q; ++t)
-#pragma unroll
-    for (int i = 0; i < NPT; ++i) q[t][i] = 0.0;
-  double cen[Q][NPT];  // CH: centre values of input planes, slot = plane % Q
-  (void)cen;
-
-  // process planes in groups of Q so the queue rotation is static
-  for (int pb = 0; pb < np; pb += Q) {
-#pragma unroll
-    for (int st = 0; st < Q; ++st) {
-      const int p = pb + st;
-      if (p < np) {
-        const int s = p % S;
-        mbar_wait(&full[s], (p / S) & 1);
-        const double* buf = ring + s * C::PLANE;
-        double sl[R + 1][NPT];
-#pragma unroll
-        for (int j = 0; j < C::PY; ++j)
-#pragma unroll
-          for (int i = 0; i < C::PX; ++i) {
-            double sv[R + 1];
-            slices_3d<R>(buf, C::PITCH, ly0 + j, lx0 + i, a.w, sv);
-            if (M == Mode::CahnHilliard) {
-              // L f'(c) with the 7-point Laplacian: in-plane part at d=0, centre at |d|=1
-              auto at = [&](int dy, int dx) { return buf[(ly0 + j + dy) * C::PITCH + lx0 + i + dx]; };
-              const double g = chem_prime(at(0, 0), a.chem);
-              const double ga = (chem_prime(at(0, -1), a.chem) + chem_prime(at(0, 1), a.chem)) +
-                                (chem_prime(at(-1, 0), a.chem) + chem_prime(at(1, 0), a.chem));
-              sv[0] = fma(a.wl1, ga, fma(a.wl0, g, sv[0]));
-              sv[1] = fma(a.wl1, g, sv[1]);
-            }
-#pragma unroll
-            for (int d = 0; d <= R; ++d) sl[d][j * C::PX + i] = sv[d];
-          }
-        // centre values needed by the CH update of the output plane p - R
-        double cz_now[NPT];
-        if (M == Mode::CahnHilliard) {
-#pragma unroll
-          for (int j = 0; j < C::PY; ++j)
-#pragma unroll
-            for (int i = 0; i < C::PX; ++i) cz_now[j * C::PX + i] = buf[(ly0 + j) * C::PITCH + lx0 + i];
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        // push: input plane p feeds output o = p - R - dz, queue slot t = R - dz
-#pragma unroll
-        for (int t = 0; t < Q; ++t) {
-          const int d = t < R ? R - t : t - R;
-          const int slot = (st + t) % Q;
-#pragma unroll
-          for (int i = 0; i < NPT; ++i) q[slot][i] += sl[d][i];
-        }
-        if (M == Mode::CahnHilliard) {
-          // input plane p is output plane p - R: keep its centre values until complete
-#pragma unroll
-          for (int i = 0; i < NPT; ++i) cen[st][i] = cz_now[i];
-        }
-        // output o = p - 2R (queue slot t = 0) is complete
-        const int o = p - 2 * R;
-        const int slot0 = st % Q;
-        if (o >= 0) {
-          const int64_t gz = z0 + o;
-          double* outp = a.v + (gz * a.ny) * a.nx;
-#pragma unroll
-          for (int j = 0; j < C::PY; ++j) {
-            const int64_t gy = y0 + ty * C::PY + j;
-            if (gy >= a.ny) continue;
-            double val[C::PX];
-#pragma unroll
-            for (int i = 0; i < C::PX; ++i) {
-              val[i] = q[slot0][j * C::PX + i];
-              if (M == Mode::CahnHilliard) val[i] += cen[(st + R + 1) % Q][j * C::PX + i];
-            }
-            double* dst = outp + gy * a.nx + gx0;
-            if (a.bulk_ok && C::PX % 2 == 0 && gx0 + C::PX <= a.nx) {
-#pragma unroll
-              for (int i = 0; i < C::PX; i += 2) store_f64x2<M>(dst + i, val[i], val[i + 1]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < C::PX; ++i)
-                if (gx0 + i < a.nx) dst[i] = val[i];
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < NPT; ++i) q[slot0][i] = 0.0;
-      }
     }
   }
 }

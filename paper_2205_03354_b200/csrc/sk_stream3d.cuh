@@ -1,0 +1,398 @@
+// 3D streaming stencil kernel (sm_100a): composed 25/73-point apply and the
+// fused explicit Cahn-Hilliard step.
+//
+// Work decomposition: the grid is cut into TX x TY column tiles; the unit of
+// work is one OUTPUT PLANE of one tile. The tiles*nz units are split into
+// gridDim.x contiguous, equal ranges (one persistent CTA per SM: a single
+// balanced wave); a range walks z inside a tile and may continue into the
+// next tile (a new "segment", whose first 2R planes re-prime the pipeline).
+//
+// Pipeline: one producer warp streams input planes ((TY+2R) x (TX+2R)
+// doubles, periodic wrap = <= 2 TMA bulk copies per row) into a STAGES-deep
+// shared-memory ring with full/empty mbarriers; 8 consumer warps evaluate the
+// stencil. Each consumer thread owns PX x PY points and, per input plane:
+//   1. loads the (PY+2R) rows of its window as 128-bit shared loads,
+//   2. accumulates in-plane ORBIT SUMS (centre, A1 = 4 axis neighbours at 1,
+//      D11 = 4 diagonals, A2, and for R=4 D21, D22, A3, A4) — the first member
+//      of each sum is assigned, the rest added, so there are no zero-inits,
+//   3. forms the R+1 slice sums S_d = sum over orbits with |dz| = d of w * sum,
+//   4. pushes them into a register queue of 2R+1 output planes (slot of an
+//      output is fixed; the rotation is static because the plane loop is
+//      unrolled by 2R+1), the deepest slot being ASSIGNED.
+// An output plane completes R planes after its own input plane; it is stored
+// with 128-bit streaming stores.
+//
+// Cahn-Hilliard mode adds, on the same loaded values, g = f'(c) as a cubic
+// polynomial (3 FMA; f'(c) = 2 rho (c-a)(c-b)(2c-a-b) expanded on the host)
+// and the 7-point Laplacian of g (S0 += wl0 g + wl1 sum_A1 g, S1 += wl1 g),
+// with B, L weights pre-scaled by -dt M kappa and dt M; output = c + queue.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sk_common.cuh"
+#include "sk_stencil_kernels.cuh"
+
+namespace sk {
+
+template <int R_, int TX_, int TY_, int PX_, int PY_, int STAGES_, int MINB_>
+struct Cfg3 {
+  static constexpr int R = R_, TX = TX_, TY = TY_, PX = PX_, PY = PY_, STAGES = STAGES_, MIN_BLOCKS = MINB_;
+  static constexpr int PITCH = TX + 2 * R;
+  static constexpr int ROWS = TY + 2 * R;
+  static constexpr int PLANE = ROWS * PITCH;  // doubles
+  static constexpr int CONSUMERS = (TX / PX) * (TY / PY);
+  static_assert(CONSUMERS % 32 == 0, "consumer threads must be whole warps");
+  static_assert(PX % 2 == 0 && R % 2 == 0, "128-bit row loads need even PX and R");
+  static constexpr int THREADS = CONSUMERS;
+  static constexpr int SMEM_BYTES = 128 + STAGES * PLANE * 8;
+  static constexpr int Q = 2 * R + 1;
+};
+
+struct Args3D {
+  const double* __restrict__ u;
+  double* __restrict__ v;
+  int64_t nx, ny, nz;
+  int tiles_x, tiles_y;
+  double w[8];       // orbit weights (pre-scaled)
+  double wl0, wl1;   // CH: 7-point Laplacian (pre-scaled by dt M)
+  Poly3 chem;        // CH: f'
+  int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
+  int64_t zchunk;    // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
+};
+
+// Unit u -> segment (tile, first plane z0, planes left in this item).
+struct Seg {
+  int64_t x0, y0, z0, len;
+};
+template <class C>
+__device__ __forceinline__ Seg seg_of(const Args3D& a, int64_t u, int64_t uend) {
+  const int64_t item = u / a.zchunk, k = u - item * a.zchunk;
+  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
+  const int64_t zc = item / tiles, tile = item - zc * tiles;
+  Seg s;
+  s.z0 = zc * a.zchunk + k;
+  s.len = a.zchunk - k < uend - u ? a.zchunk - k : uend - u;
+  s.y0 = (tile % a.tiles_y) * C::TY;  // y fastest: y-neighbour tiles run concurrently
+  s.x0 = (tile / a.tiles_y) * C::TX;
+  return s;
+}
+
+// orbit-sum index of in-plane offset (|dx|, |dy|) at radius R; -1: not used
+template <int R>
+__host__ __device__ constexpr int kind_of(int ax, int ay) {
+  const int a = ax > ay ? ax : ay, b = ax > ay ? ay : ax;
+  if (a == 0) return 0;
+  if (a == 1 && b == 0) return 1;
+  if (a == 1 && b == 1) return 2;
+  if (a == 2 && b == 0) return 3;
+  if (R >= 4) {
+    if (a == 2 && b == 1) return 4;
+    if (a == 2 && b == 2) return 5;
+    if (a == 3 && b == 0) return 6;
+    if (a == 4 && b == 0) return 7;
+  }
+  return -1;
+}
+template <int R>
+__host__ __device__ constexpr int num_kinds() { return R >= 4 ? 8 : 4; }
+
+// Every thread of the CTA issues its share of one plane buffer as 16-byte
+// cp.async (LDGSTS, lane-parallel, deep memory-level parallelism); periodic
+// wrap per pair (pairs never straddle the wrap: nx, x0 and R are even).
+// Fallback (odd nx, tiny or unaligned grids): 8-byte copies, modulo wrap.
+// A thread's share of a plane buffer is the same set of (row, pair) slots for
+// every plane of a segment, so the wrapped in-plane source offsets are
+// computed once per segment and each plane costs one 64-bit add + LDGSTS per
+// 16-byte pair.
+template <class C>
+struct PlaneLoader {
+  static constexpr int HP = C::PITCH / 2;
+  static constexpr int NP = (C::ROWS * HP + C::THREADS - 1) / C::THREADS;
+  int src[NP];  // in-plane source offset (doubles), -1: slot unused
+  int dst[NP];  // offset in the plane buffer (doubles)
+  int64_t x0 = 0, y0 = 0;
+
+  __device__ __forceinline__ void setup(const Args3D& a, int64_t x0_, int64_t y0_) {
+    constexpr int R = C::R;
+    x0 = x0_;
+    y0 = y0_;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int i = threadIdx.x + k * C::THREADS;
+      src[k] = -1;
+      dst[k] = 0;
+      if (i < C::ROWS * HP) {
+        const int r = i / HP, c = 2 * (i - r * HP);
+        const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
+        src[k] = int(gy * a.nx + gx);
+        dst[k] = r * C::PITCH + c;
+      }
+    }
+  }
+
+  __device__ __forceinline__ void issue(double* buf, const Args3D& a, int64_t gz) const {
+    constexpr int R = C::R;
+    const double* plane = a.u + gz * a.nx * a.ny;
+    if (a.bulk_ok) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (src[k] >= 0) cp_async16(buf + dst[k], plane + src[k]);
+    } else {  // fallback: 8-byte copies, modulo wrap (odd nx, tiny or unaligned grids)
+      for (int i = threadIdx.x; i < C::PLANE; i += C::THREADS) {
+        const int r = i / C::PITCH, c = i - r * C::PITCH;
+        const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
+        cp_async8(buf + i, plane + gy * a.nx + gx);
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ double2 lds128(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+
+// Per-plane evaluation for one thread: slice sums sl[d][pt], d = 0..R, and
+// (CH) the centre values of the plane at the owned points.
+template <Mode M, class C>
+__device__ __forceinline__ void plane_slices(const double* base, const Args3D& a, double (&sl)[C::R + 1][C::PX * C::PY],
+                                             double (&cen)[C::PX * C::PY]) {
+  constexpr int R = C::R, PX = C::PX, PY = C::PY, NK = num_kinds<R>();
+  constexpr int W = PX + 2 * R;  // window width per row
+  double sums[PY][PX][NK];
+  double gc[PY][PX], ga1[PY][PX];  // CH: g at the point, sum of g over A1
+#pragma unroll
+  for (int r = -R; r < PY + R; ++r) {
+    // which columns of this row does any owned point need?
+    double row[W];
+    double grow[W];
+#pragma unroll
+    for (int k = 0; k < W; k += 2) {
+      bool need = false;
+#pragma unroll
+      for (int j = 0; j < PY; ++j)
+#pragma unroll
+        for (int i = 0; i < PX; ++i)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int dx = k + e - R - i, dy = r - j;
+            const int ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
+            if (ax <= R && ay <= R && kind_of<R>(ax, ay) >= 0) need = true;
+          }
+      if (need) {
+        const double2 v = lds128(base + r * C::PITCH + k - R);
+        row[k] = v.x;
+        row[k + 1] = v.y;
+      } else {
+        row[k] = row[k + 1] = 0.0;
+      }
+    }
+    if (M == Mode::CahnHilliard) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        bool need = false;
+#pragma unroll
+        for (int j = 0; j < PY; ++j)
+#pragma unroll
+          for (int i = 0; i < PX; ++i) {
+            const int dx = k - R - i, dy = r - j;
+            const int ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
+            if (ax + ay <= 1) need = true;
+          }
+        grow[k] = need ? poly3(row[k], a.chem) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int dy = r - j, ay = dy < 0 ? -dy : dy;
+      if (ay > R) continue;
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+#pragma unroll
+        for (int dx = -R; dx <= R; ++dx) {
+          const int ax = dx < 0 ? -dx : dx;
+          const int kd = kind_of<R>(ax, ay);
+          if (kd < 0) continue;
+          const double v = row[i + dx + R];
+          // first member of orbit (a, b), a >= b, in (dy, dx) scan order is (-a, -b)
+          const int oa = ax > ay ? ax : ay, ob = ax > ay ? ay : ax;
+          const bool first = (dy == -oa && dx == -ob);
+          if (first) sums[j][i][kd] = v;
+          else sums[j][i][kd] += v;
+          if (M == Mode::CahnHilliard) {
+            if (kd == 0) gc[j][i] = grow[i + dx + R];
+            if (kd == 1) {
+              if (first) ga1[j][i] = grow[i + dx + R];
+              else ga1[j][i] += grow[i + dx + R];
+            }
+          }
+        }
+      }
+    }
+  }
+  const double* w = a.w;
+#pragma unroll
+  for (int j = 0; j < PY; ++j)
+#pragma unroll
+    for (int i = 0; i < PX; ++i) {
+      const double* s = sums[j][i];
+      const int pt = j * PX + i;
+      cen[pt] = s[0];
+      if constexpr (R == 2) {
+        sl[0][pt] = fma(w[3], s[3], fma(w[2], s[2], fma(w[1], s[1], w[0] * s[0])));
+        sl[1][pt] = fma(w[2], s[1], w[1] * s[0]);
+        sl[2][pt] = w[3] * s[0];
+      } else {
+        sl[0][pt] = fma(w[7], s[7], fma(w[6], s[6], fma(w[5], s[5], fma(w[4], s[4], fma(w[3], s[3],
+                        fma(w[2], s[2], fma(w[1], s[1], w[0] * s[0])))))));
+        sl[1][pt] = fma(w[4], s[3], fma(w[2], s[1], w[1] * s[0]));
+        sl[2][pt] = fma(w[5], s[3], fma(w[4], s[1], w[3] * s[0]));
+        sl[3][pt] = w[6] * s[0];
+        sl[4][pt] = w[7] * s[0];
+      }
+      if (M == Mode::CahnHilliard) {
+        sl[0][pt] = fma(a.wl1, ga1[j][i], fma(a.wl0, gc[j][i], sl[0][pt]));
+        sl[1][pt] = fma(a.wl1, gc[j][i], sl[1][pt]);
+      }
+    }
+}
+
+using Cfg3R2 = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 25-point apply
+using Cfg3CH = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 3D CH (7-point L f' + 25-point B)
+using Cfg3R4 = Cfg3<4, 64, 16, 2, 2, 8, 1>;    // 73-point apply
+
+// Load cursor: walks the block's segment/plane sequence S-1 planes ahead of
+// the compute loop. The per-segment setup (64-bit divisions, wrapped source
+// offsets) is out of line so the unrolled plane loop stays lean.
+template <class C>
+struct LoadCursor {
+  int64_t u, uend, lz;
+  Seg seg;
+  PlaneLoader<C> ld;
+  int lp, np;
+  __device__ __forceinline__ void start(const Args3D& a) {
+    seg = seg_of<C>(a, u, uend);
+    ld.setup(a, seg.x0, seg.y0);
+    lz = wrap1(seg.z0 - C::R, a.nz);
+    lp = 0;
+    np = int(seg.len) + 2 * C::R;
+  }
+  __device__ __forceinline__ void issue_next(double* stage_buf, const Args3D& a) {
+    if (u < uend) {
+      ld.issue(stage_buf, a, lz);
+      lz = lz + 1 == a.nz ? 0 : lz + 1;
+      if (++lp == np) {
+        u += seg.len;
+        if (u < uend) start(a);
+      }
+    }
+    cp_async_commit();
+  }
+};
+
+template <Mode M, class C>
+__global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(const Args3D a) {
+  constexpr int R = C::R, Q = C::Q, S = C::STAGES, PX = C::PX, PY = C::PY;
+  constexpr int NPT = PX * PY;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw + 128);
+
+  // balanced contiguous range of units (see seg_of for the unit order)
+  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t per = units / G, rem = units % G;
+  const int64_t ubeg = b * per + (b < rem ? b : rem);
+  const int64_t uend = ubeg + per + (b < rem ? 1 : 0);
+
+  LoadCursor<C> lc;
+  lc.u = ubeg;
+  lc.uend = uend;
+  if (ubeg < uend) lc.start(a);
+  int s_load = 0;  // stage the load cursor fills next
+#pragma unroll 1
+  for (int k = 0; k < S - 1; ++k) {
+    lc.issue_next(ring + s_load * C::PLANE, a);
+    s_load = s_load + 1 == S ? 0 : s_load + 1;
+  }
+
+  const int tx = threadIdx.x % (C::TX / PX), ty = threadIdx.x / (C::TX / PX);
+  const int lofs = (ty * PY + R) * C::PITCH + tx * PX + R;  // first owned point in a plane buffer
+  const int64_t plane_sz = a.nx * a.ny;
+  int s_comp = 0;  // stage of the plane being computed
+  double q[Q][NPT];
+  double cen[Q][NPT];
+  (void)cen;
+  for (int64_t u = ubeg; u < uend;) {
+    const Seg sg = seg_of<C>(a, u, uend);
+    const int64_t gx0 = sg.x0 + tx * PX, gy0 = sg.y0 + ty * PY;
+    bool row_ok[PY];
+#pragma unroll
+    for (int j = 0; j < PY; ++j) row_ok[j] = gy0 + j < a.ny;
+    const bool vec_ok = a.bulk_ok && gx0 + PX <= a.nx;
+    double* outp = a.v + sg.z0 * plane_sz + gy0 * a.nx + gx0;  // output plane z0, first owned point
+    const int np = int(sg.len) + 2 * R;
+    for (int pb = 0; pb < np; pb += Q) {
+#pragma unroll
+      for (int st = 0; st < Q; ++st) {
+        const int p = pb + st;
+        if (p < np) {
+          cp_async_wait_group<S - 2>();  // this thread's copies of the plane have landed
+          __syncthreads();               // ... everyone's, and the previous plane is fully consumed
+          lc.issue_next(ring + s_load * C::PLANE, a);
+          s_load = s_load + 1 == S ? 0 : s_load + 1;
+          double sl[R + 1][NPT];
+          double cz[NPT];
+          plane_slices<M, C>(ring + s_comp * C::PLANE + lofs, a, sl, cz);
+          s_comp = s_comp + 1 == S ? 0 : s_comp + 1;
+          // input plane p feeds output o = p - R - dz at queue slot (st + t) % Q, t = R - dz;
+          // t = 2R is the deepest (first) contribution of an output: assign
+#pragma unroll
+          for (int t = 0; t < Q; ++t) {
+            const int d = t < R ? R - t : t - R;
+            const int slot = (st + t) % Q;
+#pragma unroll
+            for (int i = 0; i < NPT; ++i) {
+              if (t == 2 * R) q[slot][i] = sl[d][i];
+              else q[slot][i] += sl[d][i];
+            }
+          }
+          if (M == Mode::CahnHilliard) {
+#pragma unroll
+            for (int i = 0; i < NPT; ++i) cen[st][i] = cz[i];
+          }
+          if (p >= 2 * R) {  // output plane p - 2R is complete
+            const int slot0 = st % Q;
+#pragma unroll
+            for (int j = 0; j < PY; ++j) {
+              if (!row_ok[j]) continue;
+              double val[PX];
+#pragma unroll
+              for (int i = 0; i < PX; ++i) {
+                val[i] = q[slot0][j * PX + i];
+                if (M == Mode::CahnHilliard) val[i] += cen[(st + R + 1) % Q][j * PX + i];
+              }
+              double* dst = outp + j * a.nx;
+              if (vec_ok) {
+#pragma unroll
+                for (int i = 0; i < PX; i += 2) store_f64x2<M>(dst + i, val[i], val[i + 1]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < PX; ++i)
+                  if (gx0 + i < a.nx) dst[i] = val[i];
+              }
+            }
+            outp += plane_sz;
+          }
+        }
+      }
+    }
+    u += sg.len;
+  }
+  cp_async_wait_all();
+}
+
+}  // namespace sk
