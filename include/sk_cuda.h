@@ -82,7 +82,14 @@ typedef struct sk_ch_params {
   double rho_w;
   double c_alpha;
   double c_beta;
+  /* SK_CH_FACTORED (default): c' = c + dt M L(f'(c) - kappa L c), the
+   * composition applied as two 5/7-point passes inside one kernel;
+   * SK_CH_COMPOSED: the literal composed 13/25-point B = compose(L, L).
+   * Identical in exact arithmetic, both parity-tested against the oracle. */
+  int formulation;
 } sk_ch_params;
+
+enum sk_ch_formulation { SK_CH_FACTORED = 0, SK_CH_COMPOSED = 1 };
 
 /* SolveOptions (linalg.hpp:13-17) */
 typedef struct sk_solve_options {

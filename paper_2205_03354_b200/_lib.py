@@ -26,7 +26,11 @@ class GridDesc(C.Structure):
 
 
 class ChParams(C.Structure):
-    _fields_ = [("kappa", c_dbl), ("mobility", c_dbl), ("rho_w", c_dbl), ("c_alpha", c_dbl), ("c_beta", c_dbl)]
+    _fields_ = [("kappa", c_dbl), ("mobility", c_dbl), ("rho_w", c_dbl), ("c_alpha", c_dbl), ("c_beta", c_dbl),
+                ("formulation", c_int)]
+
+
+CH_FACTORED, CH_COMPOSED = 0, 1
 
 
 class SolveOptionsC(C.Structure):

@@ -29,16 +29,23 @@ class CahnHilliardParams:
     rho_w: float = 5.0
     c_alpha: float = 0.3
     c_beta: float = 0.7
+    # device kernel: "factored" c + dt M L(f'(c) - kappa L c) or the literal
+    # "composed" B = compose(L, L); identical in exact arithmetic
+    formulation: str = "factored"
 
     @staticmethod
-    def from_epsilon(eps: float) -> "CahnHilliardParams":
+    def from_epsilon(eps: float, formulation: str = "factored") -> "CahnHilliardParams":
         """u_t = Delta(u^3 - u - eps^2 Delta u): f'(u) = u^3 - u <=> rho_w = 1/4, c_alpha = -1, c_beta = 1."""
-        return CahnHilliardParams(kappa=eps * eps, mobility=1.0, rho_w=0.25, c_alpha=-1.0, c_beta=1.0)
+        return CahnHilliardParams(kappa=eps * eps, mobility=1.0, rho_w=0.25, c_alpha=-1.0, c_beta=1.0,
+                                  formulation=formulation)
 
     def c_struct(self) -> ChParams:
         p = ChParams()
         p.kappa, p.mobility, p.rho_w, p.c_alpha, p.c_beta = (self.kappa, self.mobility, self.rho_w, self.c_alpha,
                                                               self.c_beta)
+        if self.formulation not in ("factored", "composed"):
+            raise StencilkitError(Errc.invalid_argument, f"unknown CH formulation '{self.formulation}'")
+        p.formulation = 0 if self.formulation == "factored" else 1
         return p
 
 

@@ -18,6 +18,7 @@
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
 #include "sk_stream3d.cuh"
+#include "sk_chf3d.cuh"
 
 namespace sk {
 
@@ -136,7 +137,19 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   a.wl1 = wl1;
   a.chem = chem;
   a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R;
-  return launch_3d<Mode::CahnHilliard, C3R2>(a, stream);
+  if (p->formulation == SK_CH_COMPOSED) return launch_3d<Mode::CahnHilliard, C3R2>(a, stream);
+  // factored: mu = f' - kappa L c ; c' = c + dt M L mu
+  a.kl0 = -p->kappa * (lap->orbit_coeff[0] * sl);
+  a.kl1 = -p->kappa * (lap->orbit_coeff[1] * sl);
+  using CF = CfgChf3;
+  auto kern = chf3d_kernel<CF>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ChfSmem<CF>::BYTES);
+  if (attr != cudaSuccess) return cuda_fail(attr, "chf3d smem attribute");
+  const int64_t grid = persistent_grid<CF>(a, num_sms());
+  kern<<<unsigned(grid), CF::THREADS, ChfSmem<CF>::BYTES, stream>>>(a);
+  SK_LAUNCH_CHECK("chf3d_kernel");
+  return SK_OK;
 }
 
 }  // namespace sk
@@ -196,7 +209,8 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
   if (full > 0) {
     std::lock_guard<std::mutex> lock(g_ch_graph.mu);
     const double key_val[16] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
-                                double(g.n[0]), double(g.n[1]), double(g.n[2]), double(g.dim),
+                                double(g.n[0]), double(g.n[1]), double(g.n[2]),
+                                double(g.dim) + 10.0 * double(p->formulation),
                                 lap->orbit_coeff[0], lap->orbit_coeff[1], bilap->orbit_coeff[0],
                                 bilap->orbit_coeff[1], bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3]};
     const void* key_ptr[4] = {c, scratch, lap, bilap};

@@ -42,6 +42,8 @@ struct sk_csr {
 
 namespace sk {
 
+int num_sms();
+
 // Width checks of assemble (grid.cpp:66-75), shared by apply and assembly.
 int check_width(const sk_stencil* s, const GridInfo& g);
 

@@ -129,6 +129,7 @@ using T2 = Tile2D<64, 32, 2, 4>;
 using C3R2 = Cfg3R2;
 using C3R4 = Cfg3R4;
 
+int num_sms();
 int num_sms() {
   static int n = [] {
     int dev = 0, v = kNumSMs;
@@ -154,22 +155,7 @@ int launch_3d(Args3D a, cudaStream_t stream) {
   auto kern = stream3d_kernel<M, C>;
   static int once = set_smem(kern, C::SMEM_BYTES);
   if (once != SK_OK) return once;
-  a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
-  a.tiles_y = int((a.ny + C::TY - 1) / C::TY);
-  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
-  // persistent: MIN_BLOCKS CTAs per SM, each a balanced contiguous unit range
-  int64_t grid = int64_t(num_sms()) * C::MIN_BLOCKS;
-  if (grid > units) grid = units;
-  // z-chunk: the smallest divisor of nz covering one CTA's share, so CTAs
-  // start together at the chunk tops and neighbouring tiles advance in step
-  const int64_t share = (units + grid - 1) / grid;
-  a.zchunk = a.nz;
-  for (int64_t d = 1; d <= a.nz; ++d)
-    if (a.nz % d == 0 && d >= share) {
-      a.zchunk = d;
-      break;
-    }
-  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;  // int32 in-plane offsets
+  const int64_t grid = persistent_grid<C>(a, num_sms());
   kern<<<unsigned(grid), C::THREADS, C::SMEM_BYTES, stream>>>(a);
   SK_LAUNCH_CHECK("stream3d_kernel");
   return SK_OK;

@@ -58,10 +58,33 @@ struct Args3D {
   int tiles_x, tiles_y;
   double w[8];       // orbit weights (pre-scaled)
   double wl0, wl1;   // CH: 7-point Laplacian (pre-scaled by dt M)
+  double kl0, kl1;   // factored CH: 7-point Laplacian pre-scaled by -kappa (mu = f' - kappa L c)
   Poly3 chem;        // CH: f'
   int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
   int64_t zchunk;    // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
 };
+
+// Host: tiles, persistent grid (min_blocks CTAs per SM, each a balanced
+// contiguous unit range) and the z-chunk of the unit order.
+template <class C>
+inline int64_t persistent_grid(Args3D& a, int num_sms) {
+  a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
+  a.tiles_y = int((a.ny + C::TY - 1) / C::TY);
+  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
+  int64_t grid = int64_t(num_sms) * C::MIN_BLOCKS;
+  if (grid > units) grid = units;
+  // z-chunk: the smallest divisor of nz covering one CTA's share, so CTAs
+  // start together at the chunk tops and neighbouring tiles advance in step
+  const int64_t share = (units + grid - 1) / grid;
+  a.zchunk = a.nz;
+  for (int64_t d = 1; d <= a.nz; ++d)
+    if (a.nz % d == 0 && d >= share) {
+      a.zchunk = d;
+      break;
+    }
+  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;  // int32 in-plane offsets
+  return grid;
+}
 
 // Unit u -> segment (tile, first plane z0, planes left in this item).
 struct Seg {
@@ -104,43 +127,56 @@ __host__ __device__ constexpr int num_kinds() { return R >= 4 ? 8 : 4; }
 // wrap per pair (pairs never straddle the wrap: nx, x0 and R are even).
 // Fallback (odd nx, tiny or unaligned grids): 8-byte copies, modulo wrap.
 // A thread's share of a plane buffer is the same set of (row, pair) slots for
-// every plane of a segment, so the wrapped in-plane source offsets are
-// computed once per segment and each plane costs one 64-bit add + LDGSTS per
-// 16-byte pair.
+// every plane of a segment: the wrapped source pointers are computed once per
+// segment and advanced by one plane per issue, the shared-memory addresses
+// are precomputed, so a 16-byte pair costs an add, a 64-bit add and an LDGSTS.
 template <class C>
 struct PlaneLoader {
   static constexpr int HP = C::PITCH / 2;
   static constexpr int NP = (C::ROWS * HP + C::THREADS - 1) / C::THREADS;
-  int src[NP];  // in-plane source offset (doubles), -1: slot unused
-  int dst[NP];  // offset in the plane buffer (doubles)
+  const double* src[NP];  // source of the next plane to load
+  uint32_t dst[NP];       // shared address in stage 0 (bytes)
+  bool use[NP];
   int64_t x0 = 0, y0 = 0;
 
-  __device__ __forceinline__ void setup(const Args3D& a, int64_t x0_, int64_t y0_) {
+  // first plane to load: gz (already wrapped)
+  __device__ __forceinline__ void setup(const Args3D& a, const double* ring, int64_t x0_, int64_t y0_, int64_t gz) {
     constexpr int R = C::R;
     x0 = x0_;
     y0 = y0_;
+    const double* plane = a.u + gz * a.nx * a.ny;
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const int i = threadIdx.x + k * C::THREADS;
-      src[k] = -1;
-      dst[k] = 0;
-      if (i < C::ROWS * HP) {
+      use[k] = i < C::ROWS * HP;
+      src[k] = plane;
+      dst[k] = smem_u32(ring);
+      if (use[k]) {
         const int r = i / HP, c = 2 * (i - r * HP);
         const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
-        src[k] = int(gy * a.nx + gx);
-        dst[k] = r * C::PITCH + c;
+        src[k] = plane + gy * a.nx + gx;
+        dst[k] = smem_u32(ring + r * C::PITCH + c);
       }
     }
   }
 
-  __device__ __forceinline__ void issue(double* buf, const Args3D& a, int64_t gz) const {
+  // load the next plane (z = gz) into stage `stage`, then step the sources by
+  // one plane (back to z = 0 after the last plane: periodic z)
+  __device__ __forceinline__ void issue(double* ring, int stage, const Args3D& a, int64_t gz) {
     constexpr int R = C::R;
-    const double* plane = a.u + gz * a.nx * a.ny;
+    const int64_t psz = a.nx * a.ny;
     if (a.bulk_ok) {
+      const uint32_t soff = uint32_t(stage) * (C::PLANE * 8);
+      const int64_t step = gz + 1 == a.nz ? psz * (1 - a.nz) : psz;
 #pragma unroll
-      for (int k = 0; k < NP; ++k)
-        if (src[k] >= 0) cp_async16(buf + dst[k], plane + src[k]);
+      for (int k = 0; k < NP; ++k) {
+        if (use[k])
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst[k] + soff), "l"(src[k]) : "memory");
+        src[k] += step;
+      }
     } else {  // fallback: 8-byte copies, modulo wrap (odd nx, tiny or unaligned grids)
+      double* buf = ring + stage * C::PLANE;
+      const double* plane = a.u + gz * psz;
       for (int i = threadIdx.x; i < C::PLANE; i += C::THREADS) {
         const int r = i / C::PITCH, c = i - r * C::PITCH;
         const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
@@ -264,6 +300,7 @@ __device__ __forceinline__ void plane_slices(const double* base, const Args3D& a
 using Cfg3R2 = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 25-point apply
 using Cfg3CH = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 3D CH (7-point L f' + 25-point B)
 using Cfg3R4 = Cfg3<4, 64, 16, 2, 2, 8, 1>;    // 73-point apply
+using CfgChf3 = Cfg3<2, 64, 16, 2, 2, 6, 2>;   // factored 3D CH (sk_chf3d.cuh)
 
 // Load cursor: walks the block's segment/plane sequence S-1 planes ahead of
 // the compute loop. The per-segment setup (64-bit divisions, wrapped source
@@ -274,20 +311,20 @@ struct LoadCursor {
   Seg seg;
   PlaneLoader<C> ld;
   int lp, np;
-  __device__ __forceinline__ void start(const Args3D& a) {
+  __device__ __forceinline__ void start(const Args3D& a, const double* ring) {
     seg = seg_of<C>(a, u, uend);
-    ld.setup(a, seg.x0, seg.y0);
     lz = wrap1(seg.z0 - C::R, a.nz);
+    ld.setup(a, ring, seg.x0, seg.y0, lz);
     lp = 0;
     np = int(seg.len) + 2 * C::R;
   }
-  __device__ __forceinline__ void issue_next(double* stage_buf, const Args3D& a) {
+  __device__ __forceinline__ void issue_next(double* ring, int stage, const Args3D& a) {
     if (u < uend) {
-      ld.issue(stage_buf, a, lz);
+      ld.issue(ring, stage, a, lz);
       lz = lz + 1 == a.nz ? 0 : lz + 1;
       if (++lp == np) {
         u += seg.len;
-        if (u < uend) start(a);
+        if (u < uend) start(a, ring);
       }
     }
     cp_async_commit();
@@ -311,11 +348,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
   LoadCursor<C> lc;
   lc.u = ubeg;
   lc.uend = uend;
-  if (ubeg < uend) lc.start(a);
+  if (ubeg < uend) lc.start(a, ring);
   int s_load = 0;  // stage the load cursor fills next
 #pragma unroll 1
   for (int k = 0; k < S - 1; ++k) {
-    lc.issue_next(ring + s_load * C::PLANE, a);
+    lc.issue_next(ring, s_load, a);
     s_load = s_load + 1 == S ? 0 : s_load + 1;
   }
 
@@ -342,7 +379,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
         if (p < np) {
           cp_async_wait_group<S - 2>();  // this thread's copies of the plane have landed
           __syncthreads();               // ... everyone's, and the previous plane is fully consumed
-          lc.issue_next(ring + s_load * C::PLANE, a);
+          lc.issue_next(ring, s_load, a);
           s_load = s_load + 1 == S ? 0 : s_load + 1;
           double sl[R + 1][NPT];
           double cz[NPT];

@@ -135,9 +135,10 @@ def test_ch_2d_vs_oracle(orc, n, steps):
     assert abs(e_gpu - e_ref) <= 1e-12 * abs(e_ref)
 
 
-@pytest.mark.parametrize("n,steps", [(32, 20), (70, 5), (64, 12)])
-def test_ch_3d_vs_oracle(orc, n, steps):
-    p = CahnHilliardParams.from_epsilon(0.02)
+@pytest.mark.parametrize("formulation", ["factored", "composed"])
+@pytest.mark.parametrize("n,steps", [(32, 20), (70, 5), (64, 12), (96, 7)])
+def test_ch_3d_vs_oracle(orc, n, steps, formulation):
+    p = CahnHilliardParams.from_epsilon(0.02, formulation)
     h = 1.0 / n
     dt = 0.2 * h ** 4 / (144 * p.kappa)
     g = make_periodic_grid(3, n, h)

@@ -52,10 +52,10 @@ def main():
     if case.startswith("ch"):
         from paper_2205_03354_b200.cahn_hilliard import CahnHilliardExplicit, CahnHilliardParams
 
-        dim = 3 if case == "ch3d" else 2
+        dim = 3 if case.startswith("ch3d") else 2
         n = args.n or (256 if dim == 3 else 2048)
         eps = 0.02 if dim == 3 else 0.01
-        p = CahnHilliardParams.from_epsilon(eps)
+        p = CahnHilliardParams.from_epsilon(eps, "composed" if case.endswith("c") else "factored")
         h = 1.0 / n
         dt = (0.2 * h ** 4 / (144 * eps * eps)) if dim == 3 else (0.25 * h ** 4 / (64 * eps * eps))
         g = make_periodic_grid(dim, n, h)
