@@ -97,6 +97,15 @@ typedef struct sk_solve_options {
   int64_t max_iter;    /* <= 0: 10 * rows, as linalg.cpp:20 */
   int deflate_mean;    /* nonzero: subtract the mean of x on return */
   int check_every;     /* device iterations between host status polls (0: 64) */
+  /* Extensions (0 = reference behaviour):
+   * accept_recurrence: stop when the recurrence residual sqrt(r.r) <= tol ||b||
+   *   and report the true residual instead of requiring it (SURVEY.md §7.3:
+   *   the fp64 true-residual floor of the biharmonic exceeds 1e-10 at config
+   *   sizes, so the reference criterion cannot terminate there);
+   * use_initial_guess: start from the x passed in (nested iteration) instead
+   *   of x0 = 0 (linalg.cpp:22). */
+  int accept_recurrence;
+  int use_initial_guess;
 } sk_solve_options;
 
 typedef struct sk_solve_report {

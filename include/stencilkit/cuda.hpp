@@ -209,7 +209,7 @@ inline std::vector<double> cg_solve(const DeviceCsr& m, std::span<const double> 
   check(sk_csr_info(m.get(), &rows, &cols, nullptr, nullptr));
   if (rows != cols) throw Error(Errc::shape_mismatch, "cg_solve needs a square matrix");
   if (static_cast<int64_t>(b.size()) != rows) throw Error(Errc::shape_mismatch, "rhs length does not match matrix");
-  const sk_solve_options o{opts.rel_tol, opts.max_iter, opts.deflate_mean ? 1 : 0, 0};
+  const sk_solve_options o{opts.rel_tol, opts.max_iter, opts.deflate_mean ? 1 : 0, 0, 0, 0};
   std::vector<double> x(b.size());
   check(sk_cg_solve_host(m.get(), b.data(), x.data(), &o, report));
   return x;

@@ -34,7 +34,8 @@ CH_FACTORED, CH_COMPOSED = 0, 1
 
 
 class SolveOptionsC(C.Structure):
-    _fields_ = [("rel_tol", c_dbl), ("max_iter", c_i64), ("deflate_mean", c_int), ("check_every", c_int)]
+    _fields_ = [("rel_tol", c_dbl), ("max_iter", c_i64), ("deflate_mean", c_int), ("check_every", c_int),
+                ("accept_recurrence", c_int), ("use_initial_guess", c_int)]
 
 
 class SolveReportC(C.Structure):

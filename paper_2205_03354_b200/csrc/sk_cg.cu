@@ -21,6 +21,7 @@
 #include <string>
 
 #include "sk_internal.hpp"
+#include "sk_sell.cuh"
 
 namespace sk {
 
@@ -38,24 +39,24 @@ struct CgState {
   unsigned counter[4];
 };
 
+// Row i of M times x from the SELL-32 copy (sk_sell.cuh): reference order and rounding.
 template <class IDX>
-__device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp, const IDX* __restrict__ col,
-                                          const double* __restrict__ val, const double* __restrict__ x, int64_t i) {
-  const int64_t b = __ldg(rp + i), e = __ldg(rp + i + 1);
-  double acc = 0.0;
-  for (int64_t k = b; k < e; ++k) acc = __dadd_rn(acc, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
-  return acc;
+__device__ __forceinline__ double row_dot(const int64_t* __restrict__ sp, const int32_t* __restrict__ len,
+                                          const IDX* __restrict__ col, const double* __restrict__ val,
+                                          const double* __restrict__ x, int64_t i) {
+  return sell_row_dot(i, sp, len, col, val, x);
 }
 
 template <class IDX>
-__global__ void __launch_bounds__(kT) k1_spmv_pq(int64_t n, const int64_t* __restrict__ rp, const IDX* __restrict__ col,
-                                                 const double* __restrict__ val, const double* __restrict__ p,
-                                                 double* __restrict__ q, CgState* st, double* partials) {
+__global__ void __launch_bounds__(kT) k1_spmv_pq(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ len,
+                                                 const IDX* __restrict__ col, const double* __restrict__ val,
+                                                 const double* __restrict__ p, double* __restrict__ q, CgState* st,
+                                                 double* partials) {
   if (st->status != kRunning) return;
   __shared__ double sh[32];
   double acc = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
-    const double qi = row_dot(rp, col, val, p, i);
+    const double qi = row_dot(rp, len, col, val, p, i);
     q[i] = qi;
     acc = fma(p[i], qi, acc);
   }
@@ -107,14 +108,15 @@ __global__ void k3_xpby(int64_t n, const double* __restrict__ r, double* __restr
 
 // q = M x ; out = sum (b - q)^2   (linalg.cpp:33-39, :59-61)
 template <class IDX>
-__global__ void __launch_bounds__(kT) k_true_residual(int64_t n, const int64_t* __restrict__ rp, const IDX* __restrict__ col,
+__global__ void __launch_bounds__(kT) k_true_residual(int64_t n, const int64_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ len, const IDX* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ q, CgState* st,
                                                       double* partials) {
   __shared__ double sh[32];
   double acc = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
-    const double qi = row_dot(rp, col, val, x, i);
+    const double qi = row_dot(rp, len, col, val, x, i);
     q[i] = qi;
     const double d = __dsub_rn(b[i], qi);
     acc = fma(d, d, acc);
@@ -181,21 +183,23 @@ struct Solver {
 
   int launch_k1() {
     if (m->index_bits == 32)
-      k1_spmv_pq<int32_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int32_t*>(m->col), m->val, p, q, st,
-                                                    partials);
+      k1_spmv_pq<int32_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len, static_cast<const int32_t*>(m->sell_col),
+                                                    m->sell_val, p, q, st, partials);
     else
-      k1_spmv_pq<int64_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int64_t*>(m->col), m->val, p, q, st,
-                                                    partials);
+      k1_spmv_pq<int64_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len, static_cast<const int64_t*>(m->sell_col),
+                                                    m->sell_val, p, q, st, partials);
     SK_LAUNCH_CHECK("k1_spmv_pq");
     return SK_OK;
   }
   int true_residual(const double* x, const double* b, double* out) {
     if (m->index_bits == 32)
-      k_true_residual<int32_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int32_t*>(m->col), m->val, x,
-                                                         b, q, st, partials);
+      k_true_residual<int32_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
+                                                         static_cast<const int32_t*>(m->sell_col), m->sell_val, x, b, q,
+                                                         st, partials);
     else
-      k_true_residual<int64_t><<<grid, kT, 0, stream>>>(n, m->row_ptr, static_cast<const int64_t*>(m->col), m->val, x,
-                                                         b, q, st, partials);
+      k_true_residual<int64_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
+                                                         static_cast<const int64_t*>(m->sell_col), m->sell_val, x, b, q,
+                                                         st, partials);
     SK_LAUNCH_CHECK("k_true_residual");
     SK_CUDA_TRY(cudaMemcpyAsync(out, &st->scalar_out, sizeof(double), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -218,7 +222,7 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
              cudaStream_t stream) {
   if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
   const int64_t n = m->rows;
-  sk_solve_options opts{1e-10, 0, 0, 0};
+  sk_solve_options opts{1e-10, 0, 0, 0, 0, 0};
   if (o) opts = *o;
   const int64_t max_iter = opts.max_iter > 0 ? opts.max_iter : 10 * n;  // linalg.cpp:20
   const int check_every = opts.check_every > 0 ? opts.check_every : 64;
@@ -226,6 +230,7 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   if (rep) *rep = report;
   if (n == 0) return SK_OK;
 
+  if (int e = csr_build_sell(const_cast<sk_csr*>(m), stream)) return e;  // before any graph capture
   Solver s{m, stream, n};
   int64_t g = (n + kT - 1) / kT;
   s.grid = int(g > int64_t(kNumSMs) * 8 ? int64_t(kNumSMs) * 8 : g);
@@ -244,18 +249,32 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   s.partials = s.q + n;
   s.st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(s.partials + s.grid) + 127) & ~uintptr_t(127));
 
-  // x = 0, r = p = b (linalg.cpp:22)
-  SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
-  SK_CUDA_TRY(cudaMemcpyAsync(s.r, b, vec, cudaMemcpyDeviceToDevice, stream));
-  SK_CUDA_TRY(cudaMemcpyAsync(s.p, b, vec, cudaMemcpyDeviceToDevice, stream));
   SK_CUDA_TRY(cudaMemsetAsync(s.st, 0, sizeof(CgState), stream));
   double bb = 0;
   if (int e = s.reduce<0>(b, &bb)) return e;
   const double bnorm = std::sqrt(bb);  // :23
-  if (bnorm == 0.0) return SK_OK;      // :24
+  if (bnorm == 0.0) {                  // :24
+    SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
+    return SK_OK;
+  }
+  double rho0 = bb;
+  if (opts.use_initial_guess) {
+    // extension: r = b - M x0, p = r (the restart kernel computes exactly that)
+    double dummy = 0;
+    if (int e = s.true_residual(x, b, &dummy)) return e;
+    k_restart<<<s.grid, kT, 0, stream>>>(n, b, s.q, s.r, s.p, s.st, s.partials);
+    SK_LAUNCH_CHECK("k_restart");
+    SK_CUDA_TRY(cudaMemcpyAsync(&rho0, &s.st->rho, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    SK_CUDA_TRY(cudaStreamSynchronize(stream));
+  } else {
+    // x = 0, r = p = b (linalg.cpp:22)
+    SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
+    SK_CUDA_TRY(cudaMemcpyAsync(s.r, b, vec, cudaMemcpyDeviceToDevice, stream));
+    SK_CUDA_TRY(cudaMemcpyAsync(s.p, b, vec, cudaMemcpyDeviceToDevice, stream));
+  }
   const double target = opts.rel_tol * bnorm;
   CgState h{};
-  h.rho = bb;  // rho = r.r with r = b (:27)
+  h.rho = rho0;  // rho = r.r (:27)
   h.target = target;
   h.it = 0;
   h.max_iter = max_iter;
@@ -298,12 +317,13 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   g_launches -= 3 * check_every;  // capture does not execute
 
   int64_t restarts = 0;
-  double rho = bb;
+  double rho = rho0;
   int64_t it = 0;
   int status = kRunning;
   for (;;) {
     if (it >= max_iter) break;
     if (std::sqrt(rho) <= target) {
+      if (opts.accept_recurrence) break;  // extension: report the true residual instead
       // recurrence says converged; accept only if the true residual agrees (:31-47)
       double true_res = 0;
       if (int e = s.true_residual(x, b, &true_res)) return e;
@@ -339,7 +359,8 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   report.true_rel_residual = res / bnorm;
   report.recurrence_rel_residual = std::sqrt(rho) / bnorm;
   if (rep) *rep = report;
-  if (res > target)
+  const bool converged = opts.accept_recurrence ? std::sqrt(rho) <= target : res <= target;
+  if (!converged)
     return fail(SK_ERR_NO_CONVERGENCE, "cg stalled after " + std::to_string(it) + " iterations at relative residual " +
                                            std::to_string(res / bnorm));
   if (opts.deflate_mean) {  // :67-70
@@ -376,6 +397,9 @@ int sk_cg_solve_host(const sk_csr* m, const double* b_host, double* x_host, cons
   std::string msg;
   int st = host_roundtrip(b_host, size_t(m->rows), x_host, size_t(m->rows),
                           [&](const double* b, double* x, cudaStream_t s) {
+                            if (o && o->use_initial_guess)
+                              SK_CUDA_TRY(cudaMemcpyAsync(x, x_host, sizeof(double) * size_t(m->rows),
+                                                          cudaMemcpyHostToDevice, s));
                             solve_status = cg_solve(m, b, x, o, rep, s);
                             if (solve_status != SK_OK && solve_status != SK_ERR_NO_CONVERGENCE) return solve_status;
                             if (solve_status != SK_OK) msg = sk_last_error();

@@ -22,6 +22,8 @@
 // read at step k+1; c stage k-3 is refilled at step k).
 #pragma once
 
+#include <type_traits>
+
 #include "sk_stream3d.cuh"
 
 namespace sk {
@@ -80,8 +82,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
   const int ring_c = (ry + R) * P + rx + R;
   const int ring_m = (ry + 1) * P + rx + 2;
 
+  // Register roles are static: mu of plane j lives in M[j % 3], own c of
+  // plane j in Cc[j % 2]; the steady-state loop is unrolled by 6 (lcm) so no
+  // register is ever copied. Shared-memory stage indices rotate at run time.
+  double M[3][4], Cc[2][4];
   int s_k = 0;  // stage of c-plane k
-  double c2[4], m3[4], m2[4];  // own: c of plane k-2, mu of planes k-3, k-2
   for (int64_t u = ubeg; u < uend;) {
     const Seg sg = seg_of<C>(a, u, uend);
     const int64_t gx0 = sg.x0 + 2 * tx, gy0 = sg.y0 + 2 * ty;
@@ -89,23 +94,30 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
     const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
     double* outp = a.v + sg.z0 * plane_sz + gy0 * a.nx + gx0;
     const int np = int(sg.len) + 2 * R;
-#pragma unroll 1
-    for (int k = 0; k < np; ++k) {
+
+    // one step: plane k landed; DO_MU: mu of plane k-1; DO_OUT: output plane k-2
+    auto step = [&](auto k3_t, auto k2_t, auto mu_t, auto out_t, int k) {
+      constexpr int K3 = decltype(k3_t)::value, K2 = decltype(k2_t)::value;
+      constexpr bool DO_MU = decltype(mu_t)::value, DO_OUT = decltype(out_t)::value;
+      constexpr int I_M1 = (K3 + 2) % 3, I_M2 = (K3 + 1) % 3, I_M3 = K3;  // planes k-1, k-2, k-3
+      constexpr int I_C1 = (K2 + 1) % 2, I_C2 = K2;                      // planes k-1, k-2
       cp_async_wait_group<S - 4>();
       __syncthreads();
       lc.issue_next(ring, s_load, a);
       s_load = s_load + 1 == S ? 0 : s_load + 1;
       const int s_k1 = s_k == 0 ? S - 1 : s_k - 1;   // stage of plane k-1
       const int s_k2 = s_k1 == 0 ? S - 1 : s_k1 - 1;  // stage of plane k-2
-      double m1[4], c1[4];
-      if (k >= 2) {
-        const double* cb = ring + s_k1 * C::PLANE + cofs;   // c, plane k-1 (in-plane window)
-        const double* cn = ring + s_k * C::PLANE + cofs;    // c, plane k (z+1 centres)
+      if constexpr (DO_MU) {
+        const double* cb = ring + s_k1 * C::PLANE + cofs;  // c, plane k-1 (in-plane window)
+        const double* cn = ring + s_k * C::PLANE + cofs;   // c, plane k (z+1 centres)
         double* mb = mu_ring + ((k - 1) & 1) * SM::MU_PLANE + mofs;
         const double2 up = lds128(cb - P), dn = lds128(cb + 2 * P);
         const double2 l0 = lds128(cb - 2), o0 = lds128(cb), r0 = lds128(cb + 2);
         const double2 l1 = lds128(cb + P - 2), o1 = lds128(cb + P), r1 = lds128(cb + P + 2);
         const double2 z0n = lds128(cn), z1n = lds128(cn + P);
+        double* c1 = Cc[I_C1];
+        const double* c2 = Cc[I_C2];
+        double* m1 = M[I_M1];
         c1[0] = o0.x; c1[1] = o0.y; c1[2] = o1.x; c1[3] = o1.y;
         // 6-neighbour sums (z-1 from the register copy of plane k-2)
         double s6[4];
@@ -120,16 +132,24 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
         if (has_ring) {  // one border point of the mu tile
           const double* rb = ring + s_k1 * C::PLANE + ring_c;
           const double cc = rb[0];
-          const double s = ((ring[s_k2 * C::PLANE + ring_c] + ring[s_k * C::PLANE + ring_c]) + (rb[-1] + rb[1])) +
-                           (rb[-P] + rb[P]);
-          mu_ring[((k - 1) & 1) * SM::MU_PLANE + ring_m] = fma(a.kl1, s, fma(a.kl0, cc, poly3(cc, a.chem)));
+          const double sr = ((ring[s_k2 * C::PLANE + ring_c] + ring[s_k * C::PLANE + ring_c]) + (rb[-1] + rb[1])) +
+                            (rb[-P] + rb[P]);
+          mu_ring[((k - 1) & 1) * SM::MU_PLANE + ring_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
         }
+      } else if (K2 == 0 && K3 == 0) {  // k == 0: step 2 needs c of plane 0 (its z-1 centres)
+        const double* cb = ring + s_k * C::PLANE + cofs;
+        const double2 o0 = lds128(cb), o1 = lds128(cb + P);
+        Cc[0][0] = o0.x; Cc[0][1] = o0.y; Cc[0][2] = o1.x; Cc[0][3] = o1.y;
       }
-      if (k >= 4) {  // output plane k-2
+      if constexpr (DO_OUT) {  // output plane k-2
         const double* mb = mu_ring + (k & 1) * SM::MU_PLANE + mofs;  // slot of plane k-2
         const double2 up = lds128(mb - P), dn = lds128(mb + 2 * P);
         const double2 l0 = lds128(mb - 2), r0 = lds128(mb + 2);
         const double2 l1 = lds128(mb + P - 2), r1 = lds128(mb + P + 2);
+        const double* m1 = M[I_M1];
+        const double* m2 = M[I_M2];
+        const double* m3 = M[I_M3];
+        const double* c2 = Cc[I_C2];
         double s6[4], o[4];
         s6[0] = ((m3[0] + m1[0]) + (l0.y + m2[1])) + (up.x + m2[2]);
         s6[1] = ((m3[1] + m1[1]) + (m2[0] + r0.x)) + (up.y + m2[3]);
@@ -148,20 +168,27 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
         }
         outp += plane_sz;
       }
-      if (k >= 2) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          m3[i] = m2[i];
-          m2[i] = m1[i];
-          c2[i] = c1[i];
-        }
-      } else if (k == 0) {
-        // step 2 needs c of plane 0 (its z-1 centres) in c2
-        const double* cb = ring + s_k * C::PLANE + cofs;
-        const double2 o0 = lds128(cb), o1 = lds128(cb + P);
-        c2[0] = o0.x; c2[1] = o0.y; c2[2] = o1.x; c2[3] = o1.y;
-      }
       s_k = s_k + 1 == S ? 0 : s_k + 1;
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using T = std::true_type;
+    using F = std::false_type;
+    // prologue (np >= 5 always: len >= 1): k = 0..3
+    step(I0{}, I0{}, F{}, F{}, 0);
+    step(I1{}, I1{}, F{}, F{}, 1);
+    step(I2{}, I0{}, T{}, F{}, 2);
+    step(I0{}, I1{}, T{}, F{}, 3);
+    // steady state: k = kb + ph, kb = 4 (mod 6): k % 3 = (1 + ph) % 3, k % 2 = ph % 2
+#pragma unroll 1
+    for (int kb = 4; kb < np; kb += 6) {
+      step(I1{}, I0{}, T{}, T{}, kb);
+      if (kb + 1 < np) step(I2{}, I1{}, T{}, T{}, kb + 1);
+      if (kb + 2 < np) step(I0{}, I0{}, T{}, T{}, kb + 2);
+      if (kb + 3 < np) step(I1{}, I1{}, T{}, T{}, kb + 3);
+      if (kb + 4 < np) step(I2{}, I0{}, T{}, T{}, kb + 4);
+      if (kb + 5 < np) step(I0{}, I1{}, T{}, T{}, kb + 5);
     }
     u += sg.len;
   }

@@ -23,14 +23,92 @@
 #include <vector>
 
 #include "sk_internal.hpp"
+#include "sk_sell.cuh"
 
 sk_csr::~sk_csr() {
   if (row_ptr) cudaFree(row_ptr);
   if (col) cudaFree(col);
   if (val) cudaFree(val);
+  if (sell_ptr) cudaFree(sell_ptr);
+  if (sell_len) cudaFree(sell_len);
+  if (sell_val) cudaFree(sell_val);
+  if (sell_col) cudaFree(sell_col);
 }
 
 namespace sk {
+
+// ---- SELL-32 build (from the CSR, once per matrix) ---------------------------
+__global__ void sell_len_kernel(int64_t rows, const int64_t* __restrict__ rp, int32_t* __restrict__ len,
+                                int32_t* __restrict__ width) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int L = i < rows ? int(rp[i + 1] - rp[i]) : 0;
+  if (i < rows) len[i] = L;
+  const int w = __reduce_max_sync(0xffffffffu, unsigned(L));
+  if ((i & 31) == 0) width[i >> 5] = w;
+}
+
+template <class IDX>
+__global__ void sell_fill_kernel(int64_t rows, int64_t slices, const int64_t* __restrict__ rp,
+                                 const IDX* __restrict__ col, const double* __restrict__ val,
+                                 const int64_t* __restrict__ sp, IDX* __restrict__ scol, double* __restrict__ sval) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t s = i >> 5;
+  if (s >= slices) return;
+  const int lane = int(i & 31);
+  const int L = i < rows ? int(rp[i + 1] - rp[i]) : 0;
+  const int64_t b = i < rows ? rp[i] : 0;
+  const int W = int((sp[s + 1] - sp[s]) >> 5);
+  int64_t dst = sp[s] + lane;
+  for (int k = 0; k < W; ++k, dst += 32) {
+    sval[dst] = k < L ? val[b + k] : 0.0;
+    scol[dst] = k < L ? col[b + k] : IDX(0);
+  }
+}
+
+int csr_build_sell(sk_csr* m, cudaStream_t stream) {
+  if (m->sell_val || m->rows == 0) return SK_OK;
+  const int64_t slices = (m->rows + 31) / 32;
+  int32_t* width = nullptr;
+  SK_CUDA_TRY(cudaMalloc(&m->sell_len, sizeof(int32_t) * size_t(m->rows)));
+  SK_CUDA_TRY(cudaMalloc(&width, sizeof(int32_t) * size_t(slices)));
+  const unsigned grid = unsigned(slices * 32 / 256 + 1);
+  sell_len_kernel<<<grid, 256, 0, stream>>>(m->rows, m->row_ptr, m->sell_len, width);
+  SK_LAUNCH_CHECK("sell_len_kernel");
+  std::vector<int32_t> w(static_cast<size_t>(slices));
+  std::vector<int64_t> sp(static_cast<size_t>(slices) + 1, 0);
+  cudaError_t e = cudaMemcpyAsync(w.data(), width, sizeof(int32_t) * size_t(slices), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  cudaFree(width);
+  if (e != cudaSuccess) return cuda_fail(e, "sell widths");
+  for (int64_t s = 0; s < slices; ++s) sp[size_t(s) + 1] = sp[size_t(s)] + 32 * int64_t(w[size_t(s)]);
+  m->sell_entries = sp.back();
+  const size_t ib = size_t(m->index_bits / 8);
+  SK_CUDA_TRY(cudaMalloc(&m->sell_ptr, sizeof(int64_t) * sp.size()));
+  SK_CUDA_TRY(cudaMalloc(&m->sell_val, sizeof(double) * size_t(std::max<int64_t>(m->sell_entries, 1))));
+  SK_CUDA_TRY(cudaMalloc(&m->sell_col, ib * size_t(std::max<int64_t>(m->sell_entries, 1))));
+  SK_CUDA_TRY(cudaMemcpyAsync(m->sell_ptr, sp.data(), sizeof(int64_t) * sp.size(), cudaMemcpyHostToDevice, stream));
+  if (m->index_bits == 32)
+    sell_fill_kernel<int32_t><<<grid, 256, 0, stream>>>(m->rows, slices, m->row_ptr,
+                                                        static_cast<const int32_t*>(m->col), m->val, m->sell_ptr,
+                                                        static_cast<int32_t*>(m->sell_col), m->sell_val);
+  else
+    sell_fill_kernel<int64_t><<<grid, 256, 0, stream>>>(m->rows, slices, m->row_ptr,
+                                                        static_cast<const int64_t*>(m->col), m->val, m->sell_ptr,
+                                                        static_cast<int64_t*>(m->sell_col), m->sell_val);
+  SK_LAUNCH_CHECK("sell_fill_kernel");
+  SK_CUDA_TRY(cudaStreamSynchronize(stream));
+  return SK_OK;
+}
+
+template <class IDX>
+__global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int64_t* __restrict__ sp,
+                                                        const int32_t* __restrict__ len, const IDX* __restrict__ col,
+                                                        const double* __restrict__ val, const double* __restrict__ x,
+                                                        double* __restrict__ y) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  y[i] = sell_row_dot(i, sp, len, col, val, x);
+}
 
 // ---- SpMV ------------------------------------------------------------------
 // One thread per row, entries in column order, separate multiply and add:
@@ -51,6 +129,17 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t rows, const int64_t* 
 int csr_spmv(const sk_csr* m, const double* x, double* y, cudaStream_t stream) {
   if (m->rows == 0) return SK_OK;
   const unsigned grid = unsigned((m->rows + 255) / 256);
+  if (int st = csr_build_sell(const_cast<sk_csr*>(m), stream)) return st;
+  if (m->sell_val) {
+    if (m->index_bits == 32)
+      sell_spmv_kernel<int32_t><<<grid, 256, 0, stream>>>(m->rows, m->sell_ptr, m->sell_len,
+                                                          static_cast<const int32_t*>(m->sell_col), m->sell_val, x, y);
+    else
+      sell_spmv_kernel<int64_t><<<grid, 256, 0, stream>>>(m->rows, m->sell_ptr, m->sell_len,
+                                                          static_cast<const int64_t*>(m->sell_col), m->sell_val, x, y);
+    SK_LAUNCH_CHECK("sell_spmv_kernel");
+    return SK_OK;
+  }
   if (m->index_bits == 32)
     spmv_kernel<int32_t><<<grid, 256, 0, stream>>>(m->rows, m->row_ptr, static_cast<const int32_t*>(m->col), m->val,
                                                    x, y);

@@ -37,12 +37,23 @@ struct sk_csr {
   int64_t* row_ptr = nullptr;
   void* col = nullptr;
   double* val = nullptr;
+  // SELL-32 copy used by SpMV / CG (built lazily): slices of 32 rows stored
+  // column-major, so "thread = row, entry k" loads are coalesced while each
+  // row is still summed sequentially in column order (bit-identical to CSR).
+  int64_t* sell_ptr = nullptr;  // [slices + 1] first entry of each slice
+  int32_t* sell_len = nullptr;  // [rows] row lengths
+  double* sell_val = nullptr;
+  void* sell_col = nullptr;     // int32 or int64 (index_bits)
+  int64_t sell_entries = 0;
   ~sk_csr();
 };
 
 namespace sk {
 
 int num_sms();
+
+// Build the SELL-32 copy of a CSR (idempotent; not capturable: call before graph capture).
+int csr_build_sell(sk_csr* m, cudaStream_t stream);
 
 // Width checks of assemble (grid.cpp:66-75), shared by apply and assembly.
 int check_width(const sk_stencil* s, const GridInfo& g);

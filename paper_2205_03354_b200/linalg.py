@@ -18,6 +18,9 @@ class SolveOptions:
     max_iter: int = 0          # 0: 10 * unknown count
     deflate_mean: bool = False
     check_every: int = 64      # device iterations per host status poll
+    # extensions (off = reference semantics, linalg.cpp:15-72)
+    accept_recurrence: bool = False  # stop on sqrt(r.r) <= tol ||b||, report the true residual
+    use_initial_guess: bool = False  # start from x_out's contents instead of x0 = 0
 
 
 @dataclass
@@ -34,6 +37,8 @@ def _opts(o: SolveOptions) -> SolveOptionsC:
     c.max_iter = o.max_iter
     c.deflate_mean = 1 if o.deflate_mean else 0
     c.check_every = o.check_every
+    c.accept_recurrence = 1 if o.accept_recurrence else 0
+    c.use_initial_guess = 1 if o.use_initial_guess else 0
     return c
 
 

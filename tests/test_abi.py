@@ -76,5 +76,5 @@ def test_struct_layouts_match_header():
     # sk_grid_desc {int; int64[3]; double; int[3]} with natural alignment
     assert C.sizeof(_lib.GridDesc) == 4 + 4 + 24 + 8 + 12 + 4
     assert C.sizeof(_lib.ChParams) == 5 * 8 + 8
-    assert C.sizeof(_lib.SolveOptionsC) == 8 + 8 + 4 + 4
+    assert C.sizeof(_lib.SolveOptionsC) == 8 + 8 + 4 + 4 + 4 + 4
     assert C.sizeof(_lib.SolveReportC) == 32
