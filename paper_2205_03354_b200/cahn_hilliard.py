@@ -43,9 +43,10 @@ class CahnHilliardParams:
         p = ChParams()
         p.kappa, p.mobility, p.rho_w, p.c_alpha, p.c_beta = (self.kappa, self.mobility, self.rho_w, self.c_alpha,
                                                               self.c_beta)
-        if self.formulation not in ("factored", "composed"):
+        codes = {"factored": 0, "composed": 1, "probe-copy": 2}  # probe-copy: data-movement ceiling, not a CH step
+        if self.formulation not in codes:
             raise StencilkitError(Errc.invalid_argument, f"unknown CH formulation '{self.formulation}'")
-        p.formulation = 0 if self.formulation == "factored" else 1
+        p.formulation = codes[self.formulation]
         return p
 
 

@@ -10,7 +10,7 @@
 // Delta(u^3 - u - eps^2 Delta u) fused into one pass.
 //
 // Streaming along z (per CTA: one TX x TY column tile over a z-range, the
-// persistent balanced unit order of sk_stream3d.cuh):
+// unit schedule of sk_stream3d.cuh):
 //   step k : c-plane k has landed (multistage cp.async ring, S stages)
 //            -> mu of plane k-1 on the tile + a 1-point ring (c planes
 //               k-2, k-1, k), own points from 128-bit loads, ring points by
@@ -19,7 +19,9 @@
 //               thread's own mu of planes k-3, k-1 (registers), + c of
 //               plane k-2 (register), streamed out with 128-bit stores.
 // One __syncthreads per plane orders everything (mu slot written at step k is
-// read at step k+1; c stage k-3 is refilled at step k).
+// read at step k+1; c stage k-3 is refilled at step k). Each thread owns
+// 2 rows x PX columns; register roles are static (mu of plane j in M[j % 3],
+// own c of plane j in Cc[j % 2], loop unrolled by 6), so no register moves.
 #pragma once
 
 #include <type_traits>
@@ -30,27 +32,33 @@ namespace sk {
 
 template <class C>
 struct ChfSmem {
-  static constexpr int MU_ROWS = C::TY + 2;          // y in [-1, TY]
+  static constexpr int MU_ROWS = C::TY + 2;            // y in [-1, TY]
   static constexpr int MU_PLANE = MU_ROWS * C::PITCH;  // x at column x + 2 (interior 16B aligned)
   static constexpr int BYTES = 128 + (C::STAGES * C::PLANE + 2 * MU_PLANE) * 8;
   static constexpr int RING_PTS = 2 * (C::TX + 2) + 2 * C::TY;  // the 1-point border
+  static constexpr int RING_PER_THREAD = (RING_PTS + C::THREADS - 1) / C::THREADS;
 };
 
-template <class C>
+// V = 0: the step. V = 1 (profiling only): same pipeline, loads and stores,
+// no stencil arithmetic (the data-movement ceiling of this design).
+template <class C, int V = 0>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const Args3D a) {
-  constexpr int R = 2, S = C::STAGES, P = C::PITCH;
-  static_assert(C::R == 2 && C::PX == 2 && C::PY == 2, "factored CH kernel layout");
+  constexpr int R = 2, S = C::STAGES, P = C::PITCH, PX = C::PX, NP = 2 * PX;
+  constexpr int W = PX + 4;  // in-row window x-2 .. x+PX+1
+  static_assert(C::R == 2 && C::PY == 2 && (PX == 2 || PX == 4), "factored CH kernel layout");
   using SM = ChfSmem<C>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw + 128);
   double* mu_ring = ring + S * C::PLANE;
 
+  // static balanced schedule: a contiguous range of (z-chunk, tile, z) units
+  // per CTA (measured faster than the dynamic item queue for this
+  // issue-bound kernel: no per-item pipeline re-priming)
   const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
   const int64_t G = gridDim.x, b = blockIdx.x;
   const int64_t per = units / G, rem = units % G;
   const int64_t ubeg = b * per + (b < rem ? b : rem);
   const int64_t uend = ubeg + per + (b < rem ? 1 : 0);
-
   LoadCursor<C> lc;
   lc.u = ubeg;
   lc.uend = uend;
@@ -62,36 +70,34 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
     s_load = s_load + 1 == S ? 0 : s_load + 1;
   }
 
-  const int tx = threadIdx.x % (C::TX / 2), ty = threadIdx.x / (C::TX / 2);
-  const int cofs = (2 * ty + R) * P + 2 * tx + R;  // own point (x, y) in a c buffer
-  const int mofs = (2 * ty + 1) * P + 2 * tx + 2;  // own point in a mu buffer
+  const int tx = threadIdx.x % (C::TX / PX), ty = threadIdx.x / (C::TX / PX);
+  const int cofs = (2 * ty + R) * P + PX * tx + R;  // own point (x, y) in a c buffer
+  const int mofs = (2 * ty + 1) * P + PX * tx + 2;  // own point in a mu buffer
   const int64_t plane_sz = a.nx * a.ny;
-  // ring point handled by this thread (if any): its coordinates in tile space
-  int rx = 0, ry = 0;
-  // border points on the first RING_PTS threads (consecutive lanes on
-  // consecutive shared-memory words; measured faster than spreading them)
-  const int ring_i = threadIdx.x;
-  const bool has_ring = ring_i < SM::RING_PTS;
-  {
-    const int i = ring_i;
+  // border points of the mu tile: point i on thread i % THREADS
+  int ring_c[SM::RING_PER_THREAD], ring_m[SM::RING_PER_THREAD];
+  bool has_ring[SM::RING_PER_THREAD];
+#pragma unroll
+  for (int q = 0; q < SM::RING_PER_THREAD; ++q) {
+    const int i = threadIdx.x + q * C::THREADS;
+    int rx, ry;
     if (i < C::TX + 2) { rx = i - 1; ry = -1; }
     else if (i < 2 * (C::TX + 2)) { rx = i - (C::TX + 2) - 1; ry = C::TY; }
     else if (i < 2 * (C::TX + 2) + C::TY) { rx = -1; ry = i - 2 * (C::TX + 2); }
     else { rx = C::TX; ry = i - 2 * (C::TX + 2) - C::TY; }
+    has_ring[q] = i < SM::RING_PTS;
+    ring_c[q] = (ry + R) * P + rx + R;
+    ring_m[q] = (ry + 1) * P + rx + 2;
   }
-  const int ring_c = (ry + R) * P + rx + R;
-  const int ring_m = (ry + 1) * P + rx + 2;
 
-  // Register roles are static: mu of plane j lives in M[j % 3], own c of
-  // plane j in Cc[j % 2]; the steady-state loop is unrolled by 6 (lcm) so no
-  // register is ever copied. Shared-memory stage indices rotate at run time.
-  double M[3][4], Cc[2][4];
-  int s_k = 0;  // stage of c-plane k
-  for (int64_t u = ubeg; u < uend;) {
+  double M[3][NP], Cc[2][NP];  // own points: j * PX + i (row j, column i)
+  int s_k = 0;                 // stage of c-plane k
+  for (int64_t u = ubeg; u < uend; ) {
     const Seg sg = seg_of<C>(a, u, uend);
-    const int64_t gx0 = sg.x0 + 2 * tx, gy0 = sg.y0 + 2 * ty;
+    u += sg.len;
+    const int64_t gx0 = sg.x0 + PX * tx, gy0 = sg.y0 + 2 * ty;
     const bool row0 = gy0 < a.ny, row1 = gy0 + 1 < a.ny;
-    const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
+    const bool vec_ok = a.bulk_ok && gx0 + PX <= a.nx;
     double* outp = a.v + sg.z0 * plane_sz + gy0 * a.nx + gx0;
     const int np = int(sg.len) + 2 * R;
 
@@ -107,64 +113,113 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
       s_load = s_load + 1 == S ? 0 : s_load + 1;
       const int s_k1 = s_k == 0 ? S - 1 : s_k - 1;   // stage of plane k-1
       const int s_k2 = s_k1 == 0 ? S - 1 : s_k1 - 1;  // stage of plane k-2
-      if constexpr (DO_MU) {
+      if constexpr (DO_MU && V == 1) {
+        const double* cb = ring + s_k1 * C::PLANE + cofs;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int m = 0; m < PX; m += 2) {
+            const double2 o = lds128(cb + j * P + m);
+            Cc[I_C1][j * PX + m] = M[I_M1][j * PX + m] = o.x;
+            Cc[I_C1][j * PX + m + 1] = M[I_M1][j * PX + m + 1] = o.y;
+          }
+      } else if constexpr (DO_MU) {
         const double* cb = ring + s_k1 * C::PLANE + cofs;  // c, plane k-1 (in-plane window)
         const double* cn = ring + s_k * C::PLANE + cofs;   // c, plane k (z+1 centres)
         double* mb = mu_ring + ((k - 1) & 1) * SM::MU_PLANE + mofs;
-        const double2 up = lds128(cb - P), dn = lds128(cb + 2 * P);
-        const double2 l0 = lds128(cb - 2), o0 = lds128(cb), r0 = lds128(cb + 2);
-        const double2 l1 = lds128(cb + P - 2), o1 = lds128(cb + P), r1 = lds128(cb + P + 2);
-        const double2 z0n = lds128(cn), z1n = lds128(cn + P);
+        double w0[W], w1[W], up[PX], dn[PX], z0[PX], z1[PX];
+#pragma unroll
+        for (int m = 0; m < W; m += 2) {
+          const double2 a0 = lds128(cb + m - 2), a1 = lds128(cb + P + m - 2);
+          w0[m] = a0.x; w0[m + 1] = a0.y; w1[m] = a1.x; w1[m + 1] = a1.y;
+        }
+#pragma unroll
+        for (int m = 0; m < PX; m += 2) {
+          const double2 u2 = lds128(cb - P + m), d2 = lds128(cb + 2 * P + m);
+          const double2 za = lds128(cn + m), zb = lds128(cn + P + m);
+          up[m] = u2.x; up[m + 1] = u2.y; dn[m] = d2.x; dn[m + 1] = d2.y;
+          z0[m] = za.x; z0[m + 1] = za.y; z1[m] = zb.x; z1[m + 1] = zb.y;
+        }
         double* c1 = Cc[I_C1];
         const double* c2 = Cc[I_C2];
         double* m1 = M[I_M1];
-        c1[0] = o0.x; c1[1] = o0.y; c1[2] = o1.x; c1[3] = o1.y;
-        // 6-neighbour sums (z-1 from the register copy of plane k-2)
-        double s6[4];
-        s6[0] = ((c2[0] + z0n.x) + (l0.y + o0.y)) + (up.x + o1.x);
-        s6[1] = ((c2[1] + z0n.y) + (o0.x + r0.x)) + (up.y + o1.y);
-        s6[2] = ((c2[2] + z1n.x) + (l1.y + o1.y)) + (o0.x + dn.x);
-        s6[3] = ((c2[3] + z1n.y) + (o1.x + r1.x)) + (o0.y + dn.y);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) m1[i] = fma(a.kl1, s6[i], fma(a.kl0, c1[i], poly3(c1[i], a.chem)));
-        *reinterpret_cast<double2*>(mb) = make_double2(m1[0], m1[1]);
-        *reinterpret_cast<double2*>(mb + P) = make_double2(m1[2], m1[3]);
-        if (has_ring) {  // one border point of the mu tile
-          const double* rb = ring + s_k1 * C::PLANE + ring_c;
-          const double cc = rb[0];
-          const double sr = ((ring[s_k2 * C::PLANE + ring_c] + ring[s_k * C::PLANE + ring_c]) + (rb[-1] + rb[1])) +
-                            (rb[-P] + rb[P]);
-          mu_ring[((k - 1) & 1) * SM::MU_PLANE + ring_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
+        for (int i = 0; i < PX; ++i) {
+          c1[i] = w0[i + 2];
+          c1[PX + i] = w1[i + 2];
+          // 6-neighbour sums: ((z-1 + z+1) + (left + right)) + (up + down)
+          const double s0 = ((c2[i] + z0[i]) + (w0[i + 1] + w0[i + 3])) + (up[i] + w1[i + 2]);
+          const double s1 = ((c2[PX + i] + z1[i]) + (w1[i + 1] + w1[i + 3])) + (w0[i + 2] + dn[i]);
+          m1[i] = fma(a.kl1, s0, fma(a.kl0, c1[i], poly3(c1[i], a.chem)));
+          m1[PX + i] = fma(a.kl1, s1, fma(a.kl0, c1[PX + i], poly3(c1[PX + i], a.chem)));
+        }
+#pragma unroll
+        for (int m = 0; m < PX; m += 2) {
+          *reinterpret_cast<double2*>(mb + m) = make_double2(m1[m], m1[m + 1]);
+          *reinterpret_cast<double2*>(mb + P + m) = make_double2(m1[PX + m], m1[PX + m + 1]);
+        }
+#pragma unroll
+        for (int q = 0; q < SM::RING_PER_THREAD; ++q) {
+          if (has_ring[q]) {  // one border point of the mu tile
+            const double* rb = ring + s_k1 * C::PLANE + ring_c[q];
+            const double cc = rb[0];
+            const double sr = ((ring[s_k2 * C::PLANE + ring_c[q]] + ring[s_k * C::PLANE + ring_c[q]]) +
+                               (rb[-1] + rb[1])) + (rb[-P] + rb[P]);
+            mu_ring[((k - 1) & 1) * SM::MU_PLANE + ring_m[q]] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
+          }
         }
       } else if (K2 == 0 && K3 == 0) {  // k == 0: step 2 needs c of plane 0 (its z-1 centres)
         const double* cb = ring + s_k * C::PLANE + cofs;
-        const double2 o0 = lds128(cb), o1 = lds128(cb + P);
-        Cc[0][0] = o0.x; Cc[0][1] = o0.y; Cc[0][2] = o1.x; Cc[0][3] = o1.y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int m = 0; m < PX; m += 2) {
+            const double2 o = lds128(cb + j * P + m);
+            Cc[0][j * PX + m] = o.x;
+            Cc[0][j * PX + m + 1] = o.y;
+          }
       }
       if constexpr (DO_OUT) {  // output plane k-2
-        const double* mb = mu_ring + (k & 1) * SM::MU_PLANE + mofs;  // slot of plane k-2
-        const double2 up = lds128(mb - P), dn = lds128(mb + 2 * P);
-        const double2 l0 = lds128(mb - 2), r0 = lds128(mb + 2);
-        const double2 l1 = lds128(mb + P - 2), r1 = lds128(mb + P + 2);
         const double* m1 = M[I_M1];
         const double* m2 = M[I_M2];
         const double* m3 = M[I_M3];
         const double* c2 = Cc[I_C2];
-        double s6[4], o[4];
-        s6[0] = ((m3[0] + m1[0]) + (l0.y + m2[1])) + (up.x + m2[2]);
-        s6[1] = ((m3[1] + m1[1]) + (m2[0] + r0.x)) + (up.y + m2[3]);
-        s6[2] = ((m3[2] + m1[2]) + (l1.y + m2[3])) + (m2[0] + dn.x);
-        s6[3] = ((m3[3] + m1[3]) + (m2[2] + r1.x)) + (m2[1] + dn.y);
+        double o[NP];
+        if constexpr (V == 1) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = fma(a.wl1, s6[i], fma(a.wl0, m2[i], c2[i]));
-        if (vec_ok) {
-          if (row0) store_f64x2<Mode::CahnHilliard>(outp, o[0], o[1]);
-          if (row1) store_f64x2<Mode::CahnHilliard>(outp + a.nx, o[2], o[3]);
+          for (int i = 0; i < NP; ++i) o[i] = c2[i];
         } else {
-          if (row0 && gx0 < a.nx) outp[0] = o[0];
-          if (row0 && gx0 + 1 < a.nx) outp[1] = o[1];
-          if (row1 && gx0 < a.nx) outp[a.nx] = o[2];
-          if (row1 && gx0 + 1 < a.nx) outp[a.nx + 1] = o[3];
+          const double* mb = mu_ring + (k & 1) * SM::MU_PLANE + mofs;  // slot of plane k-2
+          double mu[PX], md[PX];
+#pragma unroll
+          for (int m = 0; m < PX; m += 2) {
+            const double2 u2 = lds128(mb - P + m), d2 = lds128(mb + 2 * P + m);
+            mu[m] = u2.x; mu[m + 1] = u2.y; md[m] = d2.x; md[m + 1] = d2.y;
+          }
+          const double l0 = lds128(mb - 2).y, r0 = lds128(mb + PX).x;
+          const double l1 = lds128(mb + P - 2).y, r1 = lds128(mb + P + PX).x;
+#pragma unroll
+          for (int i = 0; i < PX; ++i) {
+            const double lf0 = i > 0 ? m2[i - 1] : l0, rt0 = i < PX - 1 ? m2[i + 1] : r0;
+            const double lf1 = i > 0 ? m2[PX + i - 1] : l1, rt1 = i < PX - 1 ? m2[PX + i + 1] : r1;
+            const double s0 = ((m3[i] + m1[i]) + (lf0 + rt0)) + (mu[i] + m2[PX + i]);
+            const double s1 = ((m3[PX + i] + m1[PX + i]) + (lf1 + rt1)) + (m2[i] + md[i]);
+            o[i] = fma(a.wl1, s0, fma(a.wl0, m2[i], c2[i]));
+            o[PX + i] = fma(a.wl1, s1, fma(a.wl0, m2[PX + i], c2[PX + i]));
+          }
+        }
+        if (vec_ok) {
+#pragma unroll
+          for (int m = 0; m < PX; m += 2) {
+            if (row0) store_f64x2<Mode::CahnHilliard>(outp + m, o[m], o[m + 1]);
+            if (row1) store_f64x2<Mode::CahnHilliard>(outp + a.nx + m, o[PX + m], o[PX + m + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < PX; ++i) {
+            if (row0 && gx0 + i < a.nx) outp[i] = o[i];
+            if (row1 && gx0 + i < a.nx) outp[a.nx + i] = o[PX + i];
+          }
         }
         outp += plane_sz;
       }
@@ -190,7 +245,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
       if (kb + 4 < np) step(I2{}, I0{}, T{}, T{}, kb + 4);
       if (kb + 5 < np) step(I0{}, I1{}, T{}, T{}, kb + 5);
     }
-    u += sg.len;
   }
   cp_async_wait_all();
 }

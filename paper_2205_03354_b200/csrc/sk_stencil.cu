@@ -155,7 +155,9 @@ int launch_3d(Args3D a, cudaStream_t stream) {
   auto kern = stream3d_kernel<M, C>;
   static int once = set_smem(kern, C::SMEM_BYTES);
   if (once != SK_OK) return once;
-  const int64_t grid = persistent_grid<C>(a, num_sms());
+  // lockstep for the radius-2 kernels (halo rows from L2), balanced for the
+  // issue-bound radius-4 kernel (measured at 256^3)
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/C::R == 2);
   kern<<<unsigned(grid), C::THREADS, C::SMEM_BYTES, stream>>>(a);
   SK_LAUNCH_CHECK("stream3d_kernel");
   return SK_OK;

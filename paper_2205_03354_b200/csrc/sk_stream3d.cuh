@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "sk_common.cuh"
 #include "sk_stencil_kernels.cuh"
@@ -62,19 +63,36 @@ struct Args3D {
   Poly3 chem;        // CH: f'
   int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
   int64_t zchunk;    // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
+  // dynamic schedule (chf3d): items = tiles x (nz / zchunk), claimed in order
+  unsigned long long* counter;  // zero at launch; the launch's last claim resets it
+  int64_t n_items;
 };
 
 // Host: tiles, persistent grid (min_blocks CTAs per SM, each a balanced
 // contiguous unit range) and the z-chunk of the unit order.
 template <class C>
-inline int64_t persistent_grid(Args3D& a, int num_sms) {
+inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
   a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
   a.tiles_y = int((a.ny + C::TY - 1) / C::TY);
-  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
-  int64_t grid = int64_t(num_sms) * C::MIN_BLOCKS;
-  if (grid > units) grid = units;
-  // z-chunk: the smallest divisor of nz covering one CTA's share, so CTAs
-  // start together at the chunk tops and neighbouring tiles advance in step
+  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;  // int32 in-plane offsets
+  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
+  const int64_t units = tiles * a.nz;
+  const int64_t slots = int64_t(num_sms) * C::MIN_BLOCKS;
+  int64_t grid = slots < units ? slots : units;
+  const char* sched = getenv("SK_SCHED");  // experiments: "balanced" / "lockstep" override
+  if (sched) lockstep = sched[0] == 'l';
+  if (lockstep) {
+    // lockstep: one CTA per (tile, z-chunk) with the most z-chunks
+    // that still fit one wave; every CTA starts at a chunk top, so the tiles
+    // around a halo are read at the same z at about the same time and the
+    // halo rows come from L2 instead of HBM.
+    for (int64_t k = a.nz; k >= 1; --k)
+      if (a.nz % k == 0 && tiles * k <= slots && a.nz / k >= 2 * C::R + 1) {
+        a.zchunk = a.nz / k;
+        return tiles * k;
+      }
+  }
+  // balanced: the smallest z-chunk divisor covering one CTA's equal share
   const int64_t share = (units + grid - 1) / grid;
   a.zchunk = a.nz;
   for (int64_t d = 1; d <= a.nz; ++d)
@@ -330,6 +348,95 @@ struct LoadCursor {
     cp_async_commit();
   }
 };
+
+// ---- dynamic schedule ---------------------------------------------------------
+// Items are (z-chunk, tile) pairs in z-chunk-major order, claimed one at a time
+// from a global counter just before the pipeline needs them: all CTAs work
+// on the same z-chunk at about the same time (halo rows of neighbouring tiles
+// are L2 hits) and faster SMs simply claim more items (no wave quantisation).
+__device__ __forceinline__ long long claim_item(const Args3D& a) {
+  const long long t = static_cast<long long>(atomicAdd(a.counter, 1ull));
+  // every CTA ends with exactly one failing claim: the last one resets the counter
+  if (t == a.n_items + static_cast<long long>(gridDim.x) - 1) atomicExch(a.counter, 0ull);
+  return t;
+}
+
+template <class C>
+__device__ __forceinline__ Seg item_seg(const Args3D& a, int64_t item) {
+  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
+  const int64_t zc = item / tiles, tile = item - zc * tiles;
+  Seg s;
+  s.z0 = zc * a.zchunk;
+  s.len = a.zchunk;
+  s.y0 = (tile % a.tiles_y) * C::TY;  // y fastest
+  s.x0 = (tile / a.tiles_y) * C::TX;
+  return s;
+}
+
+template <class C>
+struct DynCursor {
+  long long* s_items;  // shared ring of 4 claimed item ids, indexed by per-CTA sequence number
+  int seq = 0, lp = 0, np = 0;
+  bool active = false, switch_pending = false;
+  int64_t lz = 0;
+  PlaneLoader<C> ld;
+  __device__ __forceinline__ void start_item(const Args3D& a, const double* ring, long long item) {
+    active = item < a.n_items;
+    if (!active) return;
+    const Seg sg = item_seg<C>(a, item);
+    lz = wrap1(sg.z0 - C::R, a.nz);
+    ld.setup(a, ring, sg.x0, sg.y0, lz);
+    lp = 0;
+    np = int(sg.len) + 2 * C::R;
+  }
+  // Must be called by all threads, separated by __syncthreads.
+  __device__ __forceinline__ void issue_next(double* ring, int stage, const Args3D& a) {
+    if (switch_pending) {
+      switch_pending = false;
+      ++seq;
+      start_item(a, ring, s_items[seq & 3]);
+    }
+    if (active) {
+      ld.issue(ring, stage, a, lz);
+      lz = lz + 1 == a.nz ? 0 : lz + 1;
+      if (++lp == np) {
+        if (threadIdx.x == 0) s_items[(seq + 1) & 3] = claim_item(a);
+        switch_pending = true;
+      }
+    }
+    cp_async_commit();
+  }
+};
+
+// Host: tiles, grid and z-chunk for the dynamic schedule.
+template <class C>
+inline int64_t dynamic_grid(Args3D& a, int num_sms) {
+  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;
+  a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
+  a.tiles_y = int((a.ny + C::TY - 1) / C::TY);
+  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
+  const int64_t grid = int64_t(num_sms) * C::MIN_BLOCKS;
+  // largest z-chunk (divisor of nz, >= 8 or nz) that still gives >= 3 items per CTA
+  int64_t best = 0;
+  for (int64_t d = a.nz; d >= 1; --d)
+    if (a.nz % d == 0 && (d >= 8 || d == a.nz) && tiles * (a.nz / d) >= 3 * grid) {
+      best = d;
+      break;
+    }
+  if (best == 0)  // small grids: the smallest admissible chunk
+    for (int64_t d = 1; d <= a.nz; ++d)
+      if (a.nz % d == 0 && (d >= 8 || d == a.nz)) {
+        best = d;
+        break;
+      }
+  if (const char* zc = getenv("SK_ZCHUNK")) {
+    const int64_t v = atoll(zc);
+    if (v >= 1 && a.nz % v == 0) best = v;
+  }
+  a.zchunk = best;
+  a.n_items = tiles * (a.nz / best);
+  return grid < a.n_items ? grid : a.n_items;
+}
 
 template <Mode M, class C>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(const Args3D a) {
