@@ -41,14 +41,20 @@ namespace sk {
 template <int R_, int TX_, int TY_, int PX_, int PY_, int STAGES_, int MINB_>
 struct Cfg3 {
   static constexpr int R = R_, TX = TX_, TY = TY_, PX = PX_, PY = PY_, STAGES = STAGES_, MIN_BLOCKS = MINB_;
-  static constexpr int PITCH = TX + 2 * R;
+  static constexpr int WIDTH = TX + 2 * R;  // loaded columns x0-R .. x0+TX+R-1
   static constexpr int ROWS = TY + 2 * R;
+  // Row pitch a multiple of 128 B and column 0 at byte 128 - 8R (mod 128):
+  // with x0 % 16 == 0 and nx % 16 == 0 every 128-byte global line of a row
+  // lands in ONE 128-byte shared line, so a 16-byte cp.async warp costs 4
+  // shared wavefronts instead of ~15 (measured, ncu source page).
+  static constexpr int PITCH = (WIDTH + 15) / 16 * 16;
+  static constexpr int RING_OFS = 128 + (128 - (8 * R) % 128) % 128;  // bytes from smem base
   static constexpr int PLANE = ROWS * PITCH;  // doubles
   static constexpr int CONSUMERS = (TX / PX) * (TY / PY);
   static_assert(CONSUMERS % 32 == 0, "consumer threads must be whole warps");
   static_assert(PX % 2 == 0 && R % 2 == 0, "128-bit row loads need even PX and R");
   static constexpr int THREADS = CONSUMERS;
-  static constexpr int SMEM_BYTES = 128 + STAGES * PLANE * 8;
+  static constexpr int SMEM_BYTES = RING_OFS + STAGES * PLANE * 8;
   static constexpr int Q = 2 * R + 1;
 };
 
@@ -150,7 +156,7 @@ __host__ __device__ constexpr int num_kinds() { return R >= 4 ? 8 : 4; }
 // are precomputed, so a 16-byte pair costs an add, a 64-bit add and an LDGSTS.
 template <class C>
 struct PlaneLoader {
-  static constexpr int HP = C::PITCH / 2;
+  static constexpr int HP = C::WIDTH / 2;  // 16-byte chunks per row
   static constexpr int NP = (C::ROWS * HP + C::THREADS - 1) / C::THREADS;
   const double* src[NP];  // source of the next plane to load
   uint32_t dst[NP];       // shared address in stage 0 (bytes)
@@ -195,10 +201,10 @@ struct PlaneLoader {
     } else {  // fallback: 8-byte copies, modulo wrap (odd nx, tiny or unaligned grids)
       double* buf = ring + stage * C::PLANE;
       const double* plane = a.u + gz * psz;
-      for (int i = threadIdx.x; i < C::PLANE; i += C::THREADS) {
-        const int r = i / C::PITCH, c = i - r * C::PITCH;
+      for (int i = threadIdx.x; i < C::ROWS * C::WIDTH; i += C::THREADS) {
+        const int r = i / C::WIDTH, c = i - r * C::WIDTH;
         const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
-        cp_async8(buf + i, plane + gy * a.nx + gx);
+        cp_async8(buf + r * C::PITCH + c, plane + gy * a.nx + gx);
       }
     }
   }
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
   constexpr int R = C::R, Q = C::Q, S = C::STAGES, PX = C::PX, PY = C::PY;
   constexpr int NPT = PX * PY;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* ring = reinterpret_cast<double*>(smem_raw + 128);
+  double* ring = reinterpret_cast<double*>(smem_raw + C::RING_OFS);
 
   // balanced contiguous range of units (see seg_of for the unit order)
   const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
