@@ -151,6 +151,7 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   if (attr != cudaSuccess) return cuda_fail(attr, "chf3d smem attribute");
   // balanced static schedule (issue-bound kernel; measured 78 us vs 82 us lockstep at 256^3)
   const int64_t grid = persistent_grid<CF>(a, num_sms(), /*lockstep=*/false);
+  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   kern<<<unsigned(grid), CF::THREADS, ChfSmem<CF>::BYTES, stream>>>(a);
   SK_LAUNCH_CHECK("chf3d_kernel");
   return SK_OK;

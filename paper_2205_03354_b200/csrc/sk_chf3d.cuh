@@ -67,11 +67,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
   // static balanced schedule: a contiguous range of (z-chunk, tile, z) units
   // per CTA (measured faster than the dynamic item queue for this
   // issue-bound kernel: no per-item pipeline re-priming)
-  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
-  const int64_t G = gridDim.x, b = blockIdx.x;
-  const int64_t per = units / G, rem = units % G;
-  const int64_t ubeg = b * per + (b < rem ? b : rem);
-  const int64_t uend = ubeg + per + (b < rem ? 1 : 0);
+  const int units = a.tiles_x * a.tiles_y * int(a.nz);
+  const int G = gridDim.x, b = blockIdx.x;
+  const int per = units / G, rem = units % G;
+  const int ubeg = b * per + (b < rem ? b : rem);
+  const int uend = ubeg + per + (b < rem ? 1 : 0);
   LoadCursor<C> lc;
   lc.u = ubeg;
   lc.uend = uend;
@@ -111,14 +111,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
 
   double Cz[3][4], M[3][4];  // own c of plane j in Cz[j % 3], own mu of plane j in M[j % 3]; point 2 * row + col
   int s_k = 0;               // stage of c-plane k
-  for (int64_t u = ubeg; u < uend; ) {
+  for (int u = ubeg; u < uend; ) {
     const Seg sg = seg_of<C>(a, u, uend);
     u += sg.len;
     const int64_t gx0 = sg.x0 + 2 * lane, gy0 = sg.y0 + 2 * ty;
     const bool row0 = gy0 < a.ny, row1 = gy0 + 1 < a.ny;
     const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
-    double* outp = a.v + sg.z0 * plane_sz + gy0 * a.nx + gx0;
-    const int np = int(sg.len) + 2 * R;
+    double* outp = a.v + int64_t(sg.z0) * plane_sz + gy0 * a.nx + gx0;
+    const int np = sg.len + 2 * R;
 
     // one step: plane k landed; DO_MU: mu of plane k-1; DO_OUT: output plane k-2
     auto step = [&](auto kk_t, auto mu_t, auto out_t) {

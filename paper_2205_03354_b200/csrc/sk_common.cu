@@ -2,8 +2,6 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
-#include <map>
-#include <mutex>
 #include <random>
 #include <string>
 #include <utility>
@@ -33,22 +31,6 @@ int cuda_fail(cudaError_t e, const char* what) {
                                                                            : SK_ERR_CUDA;
   set_error(st, std::string(what) + " -> " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
   return st;
-}
-
-unsigned long long* schedule_counter(cudaStream_t stream) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> counters;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(mu);
-  auto& slot = counters[{dev, stream}];
-  if (!slot) {
-    void* p = nullptr;
-    if (cudaMalloc(&p, 64) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, 64) != cudaSuccess) return nullptr;
-    slot = static_cast<unsigned long long*>(p);
-  }
-  return slot;
 }
 
 double pow_int(double base, int exp) {  // grid.cpp:10-15

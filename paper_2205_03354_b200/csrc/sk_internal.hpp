@@ -52,10 +52,6 @@ namespace sk {
 
 int num_sms();
 
-// A zero-initialised device counter for the dynamic tile schedule, one per
-// stream (kernels on one stream run in order; each launch leaves it at zero).
-unsigned long long* schedule_counter(cudaStream_t stream);
-
 // Build the SELL-32 copy of a CSR (idempotent; not capturable: call before graph capture).
 int csr_build_sell(sk_csr* m, cudaStream_t stream);
 

@@ -68,14 +68,13 @@ struct Args3D {
   double kl0, kl1;   // factored CH: 7-point Laplacian pre-scaled by -kappa (mu = f' - kappa L c)
   Poly3 chem;        // CH: f'
   int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
-  int64_t zchunk;    // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
-  // dynamic schedule (chf3d): items = tiles x (nz / zchunk), claimed in order
-  unsigned long long* counter;  // zero at launch; the launch's last claim resets it
-  int64_t n_items;
+  int zchunk;        // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
 };
 
 // Host: tiles, persistent grid (min_blocks CTAs per SM, each a balanced
-// contiguous unit range) and the z-chunk of the unit order.
+// contiguous unit range) and the z-chunk of the unit order. Returns 0 when the
+// unit count does not fit the kernels' 32-bit unit cursor (> 2^31 tile-planes,
+// i.e. > 2^41 points: beyond any device memory).
 template <class C>
 inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
   a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
@@ -83,6 +82,7 @@ inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
   if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;  // int32 in-plane offsets
   const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
   const int64_t units = tiles * a.nz;
+  if (units >= (int64_t(1) << 31) || a.nz >= (int64_t(1) << 31)) return 0;
   const int64_t slots = int64_t(num_sms) * C::MIN_BLOCKS;
   int64_t grid = slots < units ? slots : units;
   const char* sched = getenv("SK_SCHED");  // experiments: "balanced" / "lockstep" override
@@ -94,36 +94,36 @@ inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
     // halo rows come from L2 instead of HBM.
     for (int64_t k = a.nz; k >= 1; --k)
       if (a.nz % k == 0 && tiles * k <= slots && a.nz / k >= 2 * C::R + 1) {
-        a.zchunk = a.nz / k;
+        a.zchunk = int(a.nz / k);
         return tiles * k;
       }
   }
   // balanced: the smallest z-chunk divisor covering one CTA's equal share
   const int64_t share = (units + grid - 1) / grid;
-  a.zchunk = a.nz;
+  a.zchunk = int(a.nz);
   for (int64_t d = 1; d <= a.nz; ++d)
     if (a.nz % d == 0 && d >= share) {
-      a.zchunk = d;
+      a.zchunk = int(d);
       break;
     }
-  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;  // int32 in-plane offsets
   return grid;
 }
 
 // Unit u -> segment (tile, first plane z0, planes left in this item).
 struct Seg {
-  int64_t x0, y0, z0, len;
+  int x0, y0, z0, len;
 };
 template <class C>
-__device__ __forceinline__ Seg seg_of(const Args3D& a, int64_t u, int64_t uend) {
-  const int64_t item = u / a.zchunk, k = u - item * a.zchunk;
-  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
-  const int64_t zc = item / tiles, tile = item - zc * tiles;
+__device__ __forceinline__ Seg seg_of(const Args3D& a, int u, int uend) {
+  const int item = u / a.zchunk, k = u - item * a.zchunk;
+  const int tiles = a.tiles_x * a.tiles_y;
+  const int zc = item / tiles, tile = item - zc * tiles;
+  const int ty = tile % a.tiles_y;  // y fastest: y-neighbour tiles run concurrently
   Seg s;
   s.z0 = zc * a.zchunk + k;
   s.len = a.zchunk - k < uend - u ? a.zchunk - k : uend - u;
-  s.y0 = (tile % a.tiles_y) * C::TY;  // y fastest: y-neighbour tiles run concurrently
-  s.x0 = (tile / a.tiles_y) * C::TX;
+  s.y0 = ty * C::TY;
+  s.x0 = ((tile - ty) / a.tiles_y) * C::TX;
   return s;
 }
 
@@ -158,55 +158,54 @@ template <class C>
 struct PlaneLoader {
   static constexpr int HP = C::WIDTH / 2;  // 16-byte chunks per row
   static constexpr int NP = (C::ROWS * HP + C::THREADS - 1) / C::THREADS;
-  const double* src[NP];  // source of the next plane to load
-  uint32_t dst[NP];       // shared address in stage 0 (bytes)
-  bool use[NP];
-  int64_t x0 = 0, y0 = 0;
+  const double* plane;  // the next plane to load
+  int off[NP];          // wrapped in-plane source offset of each of this thread's chunks (elements)
+  uint32_t dst[NP];     // its shared address in stage 0 (bytes)
+  int x0, y0;           // tile origin (8-byte fallback)
 
+  __device__ __forceinline__ static bool used(int k) {
+    return k + 1 < NP || int(threadIdx.x) + k * C::THREADS < C::ROWS * HP;
+  }
   // first plane to load: gz (already wrapped)
-  __device__ __forceinline__ void setup(const Args3D& a, const double* ring, int64_t x0_, int64_t y0_, int64_t gz) {
+  __device__ __forceinline__ void setup(const Args3D& a, const double* ring, int x0_, int y0_, int gz) {
     constexpr int R = C::R;
     x0 = x0_;
     y0 = y0_;
-    const double* plane = a.u + gz * a.nx * a.ny;
+    plane = a.u + int64_t(gz) * a.nx * a.ny;
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const int i = threadIdx.x + k * C::THREADS;
-      use[k] = i < C::ROWS * HP;
-      src[k] = plane;
+      off[k] = 0;
       dst[k] = smem_u32(ring);
-      if (use[k]) {
+      if (used(k)) {
         const int r = i / HP, c = 2 * (i - r * HP);
         const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
-        src[k] = plane + gy * a.nx + gx;
+        off[k] = int(gy * a.nx + gx);  // bulk path: nx * ny < 2^31
         dst[k] = smem_u32(ring + r * C::PITCH + c);
       }
     }
   }
 
-  // load the next plane (z = gz) into stage `stage`, then step the sources by
-  // one plane (back to z = 0 after the last plane: periodic z)
-  __device__ __forceinline__ void issue(double* ring, int stage, const Args3D& a, int64_t gz) {
+  // load plane `plane` (z = gz) into stage `stage`, then step to the next
+  // plane (back to z = 0 after the last one: periodic z)
+  __device__ __forceinline__ void issue(double* ring, int stage, const Args3D& a, int gz) {
     constexpr int R = C::R;
-    const int64_t psz = a.nx * a.ny;
     if (a.bulk_ok) {
       const uint32_t soff = uint32_t(stage) * (C::PLANE * 8);
-      const int64_t step = gz + 1 == a.nz ? psz * (1 - a.nz) : psz;
 #pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        if (use[k])
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst[k] + soff), "l"(src[k]) : "memory");
-        src[k] += step;
-      }
+      for (int k = 0; k < NP; ++k)
+        if (used(k))
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst[k] + soff), "l"(plane + off[k])
+                       : "memory");
     } else {  // fallback: 8-byte copies, modulo wrap (odd nx, tiny or unaligned grids)
       double* buf = ring + stage * C::PLANE;
-      const double* plane = a.u + gz * psz;
       for (int i = threadIdx.x; i < C::ROWS * C::WIDTH; i += C::THREADS) {
         const int r = i / C::WIDTH, c = i - r * C::WIDTH;
         const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
         cp_async8(buf + r * C::PITCH + c, plane + gy * a.nx + gx);
       }
     }
+    plane = gz + 1 == a.nz ? a.u : plane + a.nx * a.ny;
   }
 };
 
@@ -331,118 +330,27 @@ using CfgChf3 = Cfg3<2, 64, 16, 2, 2, 6, 2>;   // factored 3D CH (sk_chf3d.cuh)
 // offsets) is out of line so the unrolled plane loop stays lean.
 template <class C>
 struct LoadCursor {
-  int64_t u, uend, lz;
-  Seg seg;
+  int u, uend, lz, lp, np;
   PlaneLoader<C> ld;
-  int lp, np;
   __device__ __forceinline__ void start(const Args3D& a, const double* ring) {
-    seg = seg_of<C>(a, u, uend);
-    lz = wrap1(seg.z0 - C::R, a.nz);
+    const Seg seg = seg_of<C>(a, u, uend);
+    lz = seg.z0 - C::R < 0 ? seg.z0 - C::R + int(a.nz) : seg.z0 - C::R;
     ld.setup(a, ring, seg.x0, seg.y0, lz);
     lp = 0;
-    np = int(seg.len) + 2 * C::R;
+    np = seg.len + 2 * C::R;
   }
   __device__ __forceinline__ void issue_next(double* ring, int stage, const Args3D& a) {
     if (u < uend) {
       ld.issue(ring, stage, a, lz);
       lz = lz + 1 == a.nz ? 0 : lz + 1;
       if (++lp == np) {
-        u += seg.len;
+        u += np - 2 * C::R;
         if (u < uend) start(a, ring);
       }
     }
     cp_async_commit();
   }
 };
-
-// ---- dynamic schedule ---------------------------------------------------------
-// Items are (z-chunk, tile) pairs in z-chunk-major order, claimed one at a time
-// from a global counter just before the pipeline needs them: all CTAs work
-// on the same z-chunk at about the same time (halo rows of neighbouring tiles
-// are L2 hits) and faster SMs simply claim more items (no wave quantisation).
-__device__ __forceinline__ long long claim_item(const Args3D& a) {
-  const long long t = static_cast<long long>(atomicAdd(a.counter, 1ull));
-  // every CTA ends with exactly one failing claim: the last one resets the counter
-  if (t == a.n_items + static_cast<long long>(gridDim.x) - 1) atomicExch(a.counter, 0ull);
-  return t;
-}
-
-template <class C>
-__device__ __forceinline__ Seg item_seg(const Args3D& a, int64_t item) {
-  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
-  const int64_t zc = item / tiles, tile = item - zc * tiles;
-  Seg s;
-  s.z0 = zc * a.zchunk;
-  s.len = a.zchunk;
-  s.y0 = (tile % a.tiles_y) * C::TY;  // y fastest
-  s.x0 = (tile / a.tiles_y) * C::TX;
-  return s;
-}
-
-template <class C>
-struct DynCursor {
-  long long* s_items;  // shared ring of 4 claimed item ids, indexed by per-CTA sequence number
-  int seq = 0, lp = 0, np = 0;
-  bool active = false, switch_pending = false;
-  int64_t lz = 0;
-  PlaneLoader<C> ld;
-  __device__ __forceinline__ void start_item(const Args3D& a, const double* ring, long long item) {
-    active = item < a.n_items;
-    if (!active) return;
-    const Seg sg = item_seg<C>(a, item);
-    lz = wrap1(sg.z0 - C::R, a.nz);
-    ld.setup(a, ring, sg.x0, sg.y0, lz);
-    lp = 0;
-    np = int(sg.len) + 2 * C::R;
-  }
-  // Must be called by all threads, separated by __syncthreads.
-  __device__ __forceinline__ void issue_next(double* ring, int stage, const Args3D& a) {
-    if (switch_pending) {
-      switch_pending = false;
-      ++seq;
-      start_item(a, ring, s_items[seq & 3]);
-    }
-    if (active) {
-      ld.issue(ring, stage, a, lz);
-      lz = lz + 1 == a.nz ? 0 : lz + 1;
-      if (++lp == np) {
-        if (threadIdx.x == 0) s_items[(seq + 1) & 3] = claim_item(a);
-        switch_pending = true;
-      }
-    }
-    cp_async_commit();
-  }
-};
-
-// Host: tiles, grid and z-chunk for the dynamic schedule.
-template <class C>
-inline int64_t dynamic_grid(Args3D& a, int num_sms) {
-  if (a.nx * a.ny >= (int64_t(1) << 31)) a.bulk_ok = 0;
-  a.tiles_x = int((a.nx + C::TX - 1) / C::TX);
-  a.tiles_y = int((a.ny + C::TY - 1) / C::TY);
-  const int64_t tiles = int64_t(a.tiles_x) * a.tiles_y;
-  const int64_t grid = int64_t(num_sms) * C::MIN_BLOCKS;
-  // largest z-chunk (divisor of nz, >= 8 or nz) that still gives >= 3 items per CTA
-  int64_t best = 0;
-  for (int64_t d = a.nz; d >= 1; --d)
-    if (a.nz % d == 0 && (d >= 8 || d == a.nz) && tiles * (a.nz / d) >= 3 * grid) {
-      best = d;
-      break;
-    }
-  if (best == 0)  // small grids: the smallest admissible chunk
-    for (int64_t d = 1; d <= a.nz; ++d)
-      if (a.nz % d == 0 && (d >= 8 || d == a.nz)) {
-        best = d;
-        break;
-      }
-  if (const char* zc = getenv("SK_ZCHUNK")) {
-    const int64_t v = atoll(zc);
-    if (v >= 1 && a.nz % v == 0) best = v;
-  }
-  a.zchunk = best;
-  a.n_items = tiles * (a.nz / best);
-  return grid < a.n_items ? grid : a.n_items;
-}
 
 template <Mode M, class C>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(const Args3D a) {
@@ -452,11 +360,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
   double* ring = reinterpret_cast<double*>(smem_raw + C::RING_OFS);
 
   // balanced contiguous range of units (see seg_of for the unit order)
-  const int64_t units = int64_t(a.tiles_x) * a.tiles_y * a.nz;
-  const int64_t G = gridDim.x, b = blockIdx.x;
-  const int64_t per = units / G, rem = units % G;
-  const int64_t ubeg = b * per + (b < rem ? b : rem);
-  const int64_t uend = ubeg + per + (b < rem ? 1 : 0);
+  const int units = a.tiles_x * a.tiles_y * int(a.nz);
+  const int G = gridDim.x, b = blockIdx.x;
+  const int per = units / G, rem = units % G;
+  const int ubeg = b * per + (b < rem ? b : rem);
+  const int uend = ubeg + per + (b < rem ? 1 : 0);
 
   LoadCursor<C> lc;
   lc.u = ubeg;
@@ -476,14 +384,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
   double q[Q][NPT];
   double cen[Q][NPT];
   (void)cen;
-  for (int64_t u = ubeg; u < uend;) {
+  for (int u = ubeg; u < uend;) {
     const Seg sg = seg_of<C>(a, u, uend);
     const int64_t gx0 = sg.x0 + tx * PX, gy0 = sg.y0 + ty * PY;
     bool row_ok[PY];
 #pragma unroll
     for (int j = 0; j < PY; ++j) row_ok[j] = gy0 + j < a.ny;
     const bool vec_ok = a.bulk_ok && gx0 + PX <= a.nx;
-    double* outp = a.v + sg.z0 * plane_sz + gy0 * a.nx + gx0;  // output plane z0, first owned point
+    double* outp = a.v + int64_t(sg.z0) * plane_sz + gy0 * a.nx + gx0;  // output plane z0, first owned point
     const int np = int(sg.len) + 2 * R;
     for (int pb = 0; pb < np; pb += Q) {
 #pragma unroll
