@@ -46,7 +46,8 @@ def _newest_input() -> float:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = BUILD / (Path(src).stem + ".o")
-    cmd = [nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+    extra = os.environ.get("SK_NVCC_EXTRA", "").split()  # experiments, e.g. "-DSK_TMA_SPLIT=2"
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")

@@ -10,10 +10,13 @@
 // 5/7-point Laplacian, the 13/25-point composed B is summed by orbits, and
 // the update is written to the ping-pong buffer. 16 B of HBM traffic per
 // point per step (read c, write c').
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <mutex>
+#include <string>
 
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
@@ -92,8 +95,10 @@ struct ChGraph {
   std::mutex mu;
   cudaGraphExec_t exec = nullptr;
   const void* key_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
-  double key_val[16] = {};
+  double key_val[17] = {};
   int steps = 0;
+  double* pad[2] = {nullptr, nullptr};  // ghost-padded ping-pong fields of the 3D factored path
+  size_t pad_elems = 0;
 };
 ChGraph g_ch_graph;
 
@@ -101,9 +106,68 @@ constexpr int kGraphSteps = 100;  // kernels per captured graph (even: buffers r
 
 }  // namespace
 
+// Field layouts of one 3D factored step (sk_chf3d.cuh LD / OUT): inside a
+// captured chunk the field lives in ghost-padded buffers, so every step but
+// the first loads one TMA box per plane without wrap logic.
+enum ChfIo { kIoPlain = 0, kIoFirst = 1, kIoMid = 2, kIoLast = 3 };  // in/out: plain/plain, plain/pad, pad/pad, pad/plain
+
+// whole tiles of the TMA kernel, even padded rows (16 B strides), int32 in-plane offsets
+static bool chf3d_padded_ok(const GridInfo& g) {
+  using CT = CfgChf3T;
+  return g.dim == 3 && g.n[0] % CT::TX == 0 && g.n[1] % CT::TY == 0 &&
+         (g.n[0] + 2 * kPadL) * (g.n[1] + 2 * kPadT) < (int64_t(1) << 31);
+}
+
+static CUtensorMapL2promotion l2_promotion() {
+  const char* e = getenv("SK_TMA_L2");  // experiments: 0 / 64 / 128 / 256
+  const int v = e ? atoi(e) : 0;
+  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
+static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo& g) {
+  using CT = CfgChf3T;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t px = cuuint64_t(g.n[0] + 2 * kPadL), py = cuuint64_t(g.n[1] + 2 * kPadT);
+  const cuuint64_t dims[3] = {px, py, cuuint64_t(g.n[2])};
+  const cuuint64_t strides[2] = {px * 8, px * py * 8};
+  const cuuint32_t box[3] = {cuuint32_t(ChfSmem<CT, 1>::P), cuuint32_t(CT::ROWS / kTmaSplit), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return SK_OK;
+}
+
+template <class C, int V, int LD, int OUT>
+static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
+  using SM = ChfSmem<C, LD>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(chf3d_kernel<C, V, LD, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+  if (attr != cudaSuccess) return cuda_fail(attr, "chf3d smem attribute");
+  // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
+  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
+  chf3d_kernel<C, V, LD, OUT><<<unsigned(grid), C::THREADS, SM::BYTES, stream>>>(a, tm);
+  SK_LAUNCH_CHECK("chf3d_kernel");
+  return SK_OK;
+}
+
 // One fused step on the fast path (in -> out).
 static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
-                        double dt, const double* in, double* out, cudaStream_t stream, bool bulk_ok_ptrs) {
+                        double dt, const double* in, double* out, cudaStream_t stream, bool bulk_ok_ptrs,
+                        int io = kIoPlain) {
   const double dtm = dt * p->mobility;
   const double fac_b = -dtm * p->kappa;
   const double sb = pow_int(g.h, bilap->h_power), sl = pow_int(g.h, lap->h_power);
@@ -142,19 +206,21 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   a.kl0 = -p->kappa * (lap->orbit_coeff[0] * sl);
   a.kl1 = -p->kappa * (lap->orbit_coeff[1] * sl);
   using CF = CfgChf3;
-  auto kern = p->formulation == 2 ? chf3d_kernel<CF, 1> : chf3d_kernel<CF, 0>;  // 2: data-movement probe
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(chf3d_kernel<CF, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChfSmem<CF>::BYTES) ==
-              cudaSuccess
-          ? cudaFuncSetAttribute(chf3d_kernel<CF, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ChfSmem<CF>::BYTES)
-          : cudaErrorInvalidValue;
-  if (attr != cudaSuccess) return cuda_fail(attr, "chf3d smem attribute");
-  // balanced static schedule (issue-bound kernel; measured 78 us vs 82 us lockstep at 256^3)
-  const int64_t grid = persistent_grid<CF>(a, num_sms(), /*lockstep=*/false);
-  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
-  kern<<<unsigned(grid), CF::THREADS, ChfSmem<CF>::BYTES, stream>>>(a);
-  SK_LAUNCH_CHECK("chf3d_kernel");
-  return SK_OK;
+  using CT = CfgChf3T;
+  const bool probe = p->formulation == 2;  // data-movement probe (profiling)
+  CUtensorMap tm{};
+  if (io == kIoMid || io == kIoLast)
+    if (int st = make_tmap_padded(&tm, in, g)) return st;
+  switch (io) {
+    case kIoFirst:
+      return probe ? launch_chf3d<CF, 1, 0, 1>(a, tm, stream) : launch_chf3d<CF, 0, 0, 1>(a, tm, stream);
+    case kIoMid:
+      return probe ? launch_chf3d<CT, 1, 1, 1>(a, tm, stream) : launch_chf3d<CT, 0, 1, 1>(a, tm, stream);
+    case kIoLast:
+      return probe ? launch_chf3d<CT, 1, 1, 0>(a, tm, stream) : launch_chf3d<CT, 0, 1, 0>(a, tm, stream);
+    default:
+      return probe ? launch_chf3d<CF, 1, 0, 0>(a, tm, stream) : launch_chf3d<CF, 0, 0, 0>(a, tm, stream);
+  }
 }
 
 }  // namespace sk
@@ -213,25 +279,51 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
   const int64_t full = (nsteps / kGraphSteps) * kGraphSteps;
   if (full > 0) {
     std::lock_guard<std::mutex> lock(g_ch_graph.mu);
-    const double key_val[16] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
+    // 3D factored: c -> pad -> ... -> pad -> c (TMA boxes, no wrap) unless SK_CH_PADDED=0
+    const char* env_pad = getenv("SK_CH_PADDED");
+    const bool padded = g.dim == 3 && p->formulation != SK_CH_COMPOSED && ptr_ok && chf3d_padded_ok(g) &&
+                        !(env_pad && env_pad[0] == '0');
+    const double key_val[17] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
                                 double(g.n[0]), double(g.n[1]), double(g.n[2]),
                                 double(g.dim) + 10.0 * double(p->formulation),
                                 lap->orbit_coeff[0], lap->orbit_coeff[1], bilap->orbit_coeff[0],
-                                bilap->orbit_coeff[1], bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3]};
+                                bilap->orbit_coeff[1], bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3],
+                                double(padded)};
     const void* key_ptr[4] = {c, scratch, lap, bilap};
     bool hit = g_ch_graph.exec != nullptr;
     for (int i = 0; i < 4 && hit; ++i) hit = key_ptr[i] == g_ch_graph.key_ptr[i];
-    for (int i = 0; i < 16 && hit; ++i) hit = key_val[i] == g_ch_graph.key_val[i];
+    for (int i = 0; i < 17 && hit; ++i) hit = key_val[i] == g_ch_graph.key_val[i];
     if (!hit) {
       if (g_ch_graph.exec) {
         cudaGraphExecDestroy(g_ch_graph.exec);
         g_ch_graph.exec = nullptr;
       }
+      if (padded) {
+        const size_t elems = size_t(g.n[0] + 2 * kPadL) * size_t(g.n[1] + 2 * kPadT) * size_t(g.n[2]);
+        if (g_ch_graph.pad_elems != elems) {
+          for (double*& b : g_ch_graph.pad) {
+            if (b) cudaFree(b);
+            b = nullptr;
+          }
+          g_ch_graph.pad_elems = 0;
+          for (double*& b : g_ch_graph.pad) SK_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&b), elems * 8));
+          g_ch_graph.pad_elems = elems;
+        }
+      }
+      double* const* pad = g_ch_graph.pad;
       cudaStream_t cap = stream ? stream : capture_stream();
       SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       int st = SK_OK;
-      for (int k = 0; k < kGraphSteps && st == SK_OK; ++k)
-        st = ch_step_fast(lap, bilap, g, p, dt, (k % 2) ? scratch : c, (k % 2) ? c : scratch, cap, ptr_ok);
+      for (int k = 0; k < kGraphSteps && st == SK_OK; ++k) {
+        if (!padded)
+          st = ch_step_fast(lap, bilap, g, p, dt, (k % 2) ? scratch : c, (k % 2) ? c : scratch, cap, ptr_ok);
+        else if (k == 0)
+          st = ch_step_fast(lap, bilap, g, p, dt, c, pad[0], cap, ptr_ok, kIoFirst);
+        else if (k + 1 < kGraphSteps)
+          st = ch_step_fast(lap, bilap, g, p, dt, pad[(k - 1) % 2], pad[k % 2], cap, ptr_ok, kIoMid);
+        else
+          st = ch_step_fast(lap, bilap, g, p, dt, pad[(k - 1) % 2], c, cap, ptr_ok, kIoLast);
+      }
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamEndCapture(cap, &graph);
       if (st != SK_OK) {
@@ -243,7 +335,7 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
       for (int i = 0; i < 4; ++i) g_ch_graph.key_ptr[i] = key_ptr[i];
-      for (int i = 0; i < 16; ++i) g_ch_graph.key_val[i] = key_val[i];
+      for (int i = 0; i < 17; ++i) g_ch_graph.key_val[i] = key_val[i];
       g_launches -= kGraphSteps;  // capture does not execute; counted per replay below
     }
     for (int64_t k = 0; k < full; k += kGraphSteps) {

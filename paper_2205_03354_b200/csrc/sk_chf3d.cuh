@@ -30,6 +30,8 @@
 // unrolled by 3 so every register / slot role is static.
 #pragma once
 
+#include <cuda.h>
+
 #include <type_traits>
 
 #include "sk_stream3d.cuh"
@@ -40,53 +42,132 @@ namespace sk {
 // hoist it across independent work
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
-template <class C>
+// Ghost-padded field of the TMA path: row pitch nx + 2 kPadL, kPadT ghost
+// rows above and below; interior x at column x + kPadL (128 B-aligned rows
+// and tiles, so the interior stores are whole lines), ghosts x = -2, -1 and
+// nx, nx + 1 at columns kPadL - 2 .. and kPadL + nx ...
+#ifndef SK_PADL
+#define SK_PADL 16
+#endif
+constexpr int kPadL = SK_PADL, kPadT = 2;
+#ifndef SK_TMA_SPLIT
+#define SK_TMA_SPLIT 1
+#endif
+constexpr int kTmaSplit = SK_TMA_SPLIT;  // TMA boxes per plane
+
+// LD 0: cp.async ring over the caller's field (periodic wrap per chunk,
+// 128 B-aligned pitch C::PITCH). LD 1: one TMA box per plane from a
+// ghost-padded field (kPadL / kPadT below, see OUT 1) into dense stages of
+// pitch C::WIDTH; no wrap logic, no per-thread copy instructions.
+template <class C, int LD = 0>
 struct ChfSmem {
+  // LD 1 boxes start XO = 4 columns left of the tile and are 72 wide: whole
+  // 32 B sectors from the 128 B-aligned padded rows, and a 576 B pitch whose
+  // row pairs are 128 B multiples (the box may be split along y)
+  static constexpr int XO = LD ? 2 * C::R : C::R;            // column of tile x = 0 in a stage
+  static constexpr int P = LD ? C::TX + 4 * C::R : C::PITCH;  // c stage pitch
+  static constexpr int PLANE = C::ROWS * P;
+  static constexpr int RING_OFS = LD ? 128 : C::RING_OFS;  // LD 1: stage barriers in the first 128 B
+  static constexpr uint32_t STAGE_BYTES = PLANE * 8;
   static constexpr int MP = C::TX + 4;              // mu ring pitch: x in [-1, TX] at column x + 2
   static constexpr int MU_ROWS = C::TY + 2;         // y in [-1, TY]
   static constexpr int MU_PLANE = MU_ROWS * MP;
-  static constexpr int BYTES = C::RING_OFS + (C::STAGES * C::PLANE + 3 * MU_PLANE) * 8;
+  static constexpr int BYTES = RING_OFS + (C::STAGES * PLANE + 3 * MU_PLANE) * 8;
   static constexpr int WARPS = C::THREADS / 32;
   static constexpr int BORDER_ROWS = 2 * (C::TX + 2);                     // mu rows -1 and TY, x in [-1, TX]
   static constexpr int ROWS_PER_WARP = (BORDER_ROWS + WARPS - 1) / WARPS;  // + 4 side points per warp
   static_assert(ROWS_PER_WARP + 4 <= 32, "border points per warp");
+  static_assert(!LD || (STAGE_BYTES % 128 == 0 && C::STAGES * 8 <= 128), "TMA stage alignment");
+  static_assert(!LD || (C::ROWS % kTmaSplit == 0 && (C::ROWS / kTmaSplit) * P * 8 % 128 == 0), "TMA box split");
+};
+
+// TMA producer (thread 0): walks the CTA's unit range one plane ahead of
+// the consumers' needs, like LoadCursor, issuing one box per plane.
+template <class C>
+struct TmaCursor {
+  int u, uend, lp, np, x0, y0, z;
+  __device__ __forceinline__ void start(const Args3D& a) {
+    const Seg sg = seg_of<C>(a, u, uend);
+    x0 = sg.x0 + kPadL - ChfSmem<C, 1>::XO;  // padded coordinates of the box origin
+    y0 = sg.y0 + kPadT - C::R;
+    z = sg.z0 - C::R < 0 ? sg.z0 - C::R + int(a.nz) : sg.z0 - C::R;
+    lp = 0;
+    np = sg.len + 2 * C::R;
+  }
+  __device__ __forceinline__ void issue_next(double* ring, uint64_t* bars, int stage, const Args3D& a,
+                                             const CUtensorMap* tm) {
+    using SM = ChfSmem<C, 1>;
+    if (u < uend) {
+      mbar_arrive_expect_tx(&bars[stage], SM::STAGE_BYTES);
+#pragma unroll
+      for (int q = 0; q < kTmaSplit; ++q)  // the box: C::ROWS / kTmaSplit rows
+        tma_load_3d(ring + stage * SM::PLANE + q * (C::ROWS / kTmaSplit) * SM::P, tm, x0,
+                    y0 + q * (C::ROWS / kTmaSplit), z, &bars[stage]);
+      z = z + 1 == a.nz ? 0 : z + 1;
+      if (++lp == np) {
+        u += np - 2 * C::R;
+        if (u < uend) start(a);
+      }
+    }
+  }
 };
 
 // V = 0: the step. V = 1 (profiling only): same pipeline, loads and stores,
 // no stencil arithmetic (the data-movement ceiling of this design).
-template <class C, int V = 0>
-__global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const Args3D a) {
-  constexpr int R = 2, S = C::STAGES, P = C::PITCH;
+// OUT 0: write c' to a.v (nx x ny x nz). OUT 1: write c' into the interior of
+// a ghost-padded field at a.v and its periodic images into the 2-wide ghost
+// frame (the next step's TMA boxes then never wrap). LD 1 / OUT 1 need whole
+// tiles (nx % TX == 0, ny % TY == 0).
+template <class C, int V = 0, int LD = 0, int OUT = 0>
+__global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
+    chf3d_kernel(const __grid_constant__ Args3D a, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int R = 2, S = C::STAGES;
   static_assert(C::R == 2 && C::PX == 2 && C::PY == 2 && C::TX == 64, "factored CH kernel layout: warp = row pair");
-  using SM = ChfSmem<C>;
-  constexpr int MP = SM::MP;
+  using SM = ChfSmem<C, LD>;
+  constexpr int P = SM::P, PLANE = SM::PLANE, MP = SM::MP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* ring = reinterpret_cast<double*>(smem_raw + C::RING_OFS);
-  double* mu_ring = ring + S * C::PLANE;
+  double* ring = reinterpret_cast<double*>(smem_raw + SM::RING_OFS);
+  double* mu_ring = ring + S * PLANE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // LD 1: one full-barrier per stage
 
   // static balanced schedule: a contiguous range of (z-chunk, tile, z) units
-  // per CTA (measured faster than the dynamic item queue for this
-  // issue-bound kernel: no per-item pipeline re-priming)
+  // per CTA (measured faster than a dynamic item queue for this kernel)
   const int units = a.tiles_x * a.tiles_y * int(a.nz);
   const int G = gridDim.x, b = blockIdx.x;
   const int per = units / G, rem = units % G;
   const int ubeg = b * per + (b < rem ? b : rem);
   const int uend = ubeg + per + (b < rem ? 1 : 0);
   LoadCursor<C> lc;
-  lc.u = ubeg;
-  lc.uend = uend;
-  if (ubeg < uend) lc.start(a, ring);
+  TmaCursor<C> tc;
   int s_load = 0;
+  if constexpr (LD == 0) {
+    lc.u = ubeg;
+    lc.uend = uend;
+    if (ubeg < uend) lc.start(a, ring);
 #pragma unroll 1
-  for (int k = 0; k < S - 3; ++k) {
-    lc.issue_next(ring, s_load, a);
-    s_load = s_load + 1 == S ? 0 : s_load + 1;
+    for (int k = 0; k < S - 3; ++k) {
+      lc.issue_next(ring, s_load, a);
+      s_load = s_load + 1 == S ? 0 : s_load + 1;
+    }
+  } else {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc.u = ubeg;
+      tc.uend = uend;
+      if (ubeg < uend) tc.start(a);
+      for (int k = 0; k < S - 3; ++k) tc.issue_next(ring, bars, k, a, &tmap);
+    }
+    s_load = S - 3;
   }
 
   const int lane = threadIdx.x % 32, ty = threadIdx.x / 32;
-  const int cofs = (2 * ty + R) * P + 2 * lane + R;  // own point (row 0, column 0) in a c stage
+  const int cofs = (2 * ty + R) * P + 2 * lane + SM::XO;  // own point (row 0, column 0) in a c stage
   const int mofs = (2 * ty + 1) * MP + 2 * lane + 2;  // own point in a mu slot
-  const int64_t plane_sz = a.nx * a.ny;
+  const int64_t opx = OUT ? a.nx + 2 * kPadL : a.nx, opp = opx * (OUT ? a.ny + 2 * kPadT : a.ny);  // output pitches
   // one border point of the mu tile per lane (lanes < ROWS_PER_WARP: the
   // rows above / below the tile, contiguous; the next 4 lanes: the side
   // columns of this warp's row pair)
@@ -105,19 +186,29 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
       rx = sidx < 2 ? -1 : C::TX;
       ry = 2 * ty + (sidx & 1);
     }
-    ex_c = (ry + R) * P + rx + R;
+    ex_c = (ry + R) * P + rx + SM::XO;
     ex_m = (ry + 1) * MP + rx + 2;
   }
 
   double Cz[3][4], M[3][4];  // own c of plane j in Cz[j % 3], own mu of plane j in M[j % 3]; point 2 * row + col
   int s_k = 0;               // stage of c-plane k
+  uint32_t ph = 0;           // LD 1: parity of the current use of stage s_k
   for (int u = ubeg; u < uend; ) {
     const Seg sg = seg_of<C>(a, u, uend);
     u += sg.len;
     const int64_t gx0 = sg.x0 + 2 * lane, gy0 = sg.y0 + 2 * ty;
     const bool row0 = gy0 < a.ny, row1 = gy0 + 1 < a.ny;
     const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
-    double* outp = a.v + int64_t(sg.z0) * plane_sz + gy0 * a.nx + gx0;
+    double* outp = a.v + int64_t(sg.z0) * opp + (gy0 + (OUT ? kPadT : 0)) * opx + gx0 + (OUT ? kPadL : 0);
+    // OUT 1: periodic images in the ghost frame: columns 0..3 and nx-4..nx-1
+    // (whole 32 B sectors: no partial-sector writes), rows 0, 1 and ny-2, ny-1
+    const int64_t gdx_ = OUT ? (gx0 < 4 ? a.nx : (gx0 >= a.nx - 4 ? -a.nx : 0)) : 0;
+    const int64_t gdy_ = OUT ? (gy0 == 0 ? a.ny : (gy0 == a.ny - 2 ? -a.ny : 0)) * opx : 0;
+#ifdef SK_NO_GHOST  // timing experiment only (wrong results)
+    const int64_t gdx = 0 * gdx_, gdy = 0 * gdy_;
+#else
+    const int64_t gdx = gdx_, gdy = gdy_;
+#endif
     const int np = sg.len + 2 * R;
 
     // one step: plane k landed; DO_MU: mu of plane k-1; DO_OUT: output plane k-2
@@ -126,14 +217,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
       constexpr bool DO_MU = decltype(mu_t)::value, DO_OUT = decltype(out_t)::value;
       constexpr int C0 = K, C1 = (K + 2) % 3, C2 = (K + 1) % 3;  // c of planes k, k-1, k-2
       constexpr int M1 = (K + 2) % 3, M2 = (K + 1) % 3, M3 = K;  // mu of planes k-1, k-2, k-3
-      cp_async_wait_group<S - 4>();
-      __syncthreads();
-      lc.issue_next(ring, s_load, a);
+      (void)M2;
+      (void)M3;
+      if constexpr (LD == 0) {
+        cp_async_wait_group<S - 4>();
+        __syncthreads();
+        lc.issue_next(ring, s_load, a);
+      } else {
+        mbar_wait(&bars[s_k], ph);  // plane k landed
+        __syncthreads();            // ... and stage (k - 3) is free, the mu slot of plane k-2 complete
+        if (threadIdx.x == 0) {
+          fence_proxy_async_smem();
+          tc.issue_next(ring, bars, s_load, a, &tmap);
+        }
+      }
       s_load = s_load + 1 == S ? 0 : s_load + 1;
       const int s_k1 = s_k == 0 ? S - 1 : s_k - 1;   // stage of plane k-1
       const int s_k2 = s_k1 == 0 ? S - 1 : s_k1 - 1;  // stage of plane k-2
       {
-        const double* cn = ring + s_k * C::PLANE + cofs;
+        const double* cn = ring + s_k * PLANE + cofs;
         const double2 r0 = ld2(cn), r1 = ld2(cn + P);
         Cz[C0][0] = r0.x; Cz[C0][1] = r0.y; Cz[C0][2] = r1.x; Cz[C0][3] = r1.y;
       }
@@ -141,7 +243,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
 #pragma unroll
         for (int i = 0; i < 4; ++i) M[M1][i] = Cz[C1][i];
       } else if constexpr (DO_MU) {
-        const double* cb = ring + s_k1 * C::PLANE + cofs;  // c, plane k-1
+        const double* cb = ring + s_k1 * PLANE + cofs;  // c, plane k-1
         const double* c1 = Cz[C1];
         const double* zp = Cz[C0];
         const double* zm = Cz[C2];
@@ -164,9 +266,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
         *reinterpret_cast<double2*>(mb) = make_double2(m1[0], m1[1]);
         *reinterpret_cast<double2*>(mb + MP) = make_double2(m1[2], m1[3]);
         if (has_ex) {  // one border point of the mu tile
-          const double* rb = ring + s_k1 * C::PLANE + ex_c;
+          const double* rb = ring + s_k1 * PLANE + ex_c;
           const double cc = rb[0];
-          const double sr = ((ring[s_k2 * C::PLANE + ex_c] + ring[s_k * C::PLANE + ex_c]) + (rb[-1] + rb[1])) +
+          const double sr = ((ring[s_k2 * PLANE + ex_c] + ring[s_k * PLANE + ex_c]) + (rb[-1] + rb[1])) +
                             (rb[-P] + rb[P]);
           mu_ring[M1 * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
         }
@@ -196,7 +298,22 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
           o[2] = fma(a.wl1, s10, fma(a.wl0, m2[2], c2[2]));
           o[3] = fma(a.wl1, s11, fma(a.wl0, m2[3], c2[3]));
         }
-        if (vec_ok) {
+        if constexpr (OUT == 1) {  // whole tiles: every point exists
+          store_f64x2<Mode::CahnHilliard>(outp, o[0], o[1]);
+          store_f64x2<Mode::CahnHilliard>(outp + opx, o[2], o[3]);
+          if (gdx) {
+            store_f64x2<Mode::CahnHilliard>(outp + gdx, o[0], o[1]);
+            store_f64x2<Mode::CahnHilliard>(outp + gdx + opx, o[2], o[3]);
+          }
+          if (gdy) {
+            store_f64x2<Mode::CahnHilliard>(outp + gdy, o[0], o[1]);
+            store_f64x2<Mode::CahnHilliard>(outp + gdy + opx, o[2], o[3]);
+            if (gdx) {
+              store_f64x2<Mode::CahnHilliard>(outp + gdx + gdy, o[0], o[1]);
+              store_f64x2<Mode::CahnHilliard>(outp + gdx + gdy + opx, o[2], o[3]);
+            }
+          }
+        } else if (vec_ok) {
           if (row0) store_f64x2<Mode::CahnHilliard>(outp, o[0], o[1]);
           if (row1) store_f64x2<Mode::CahnHilliard>(outp + a.nx, o[2], o[3]);
         } else {
@@ -206,9 +323,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) chf3d_kernel(const 
             if (row1 && gx0 + i < a.nx) outp[a.nx + i] = o[2 + i];
           }
         }
-        outp += plane_sz;
+        outp += opp;
       }
-      s_k = s_k + 1 == S ? 0 : s_k + 1;
+      if (++s_k == S) {
+        s_k = 0;
+        ph ^= 1u;
+      }
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;

@@ -323,7 +323,8 @@ __device__ __forceinline__ void plane_slices(const double* base, const Args3D& a
 using Cfg3R2 = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 25-point apply
 using Cfg3CH = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 3D CH (7-point L f' + 25-point B)
 using Cfg3R4 = Cfg3<4, 64, 16, 2, 2, 8, 1>;    // 73-point apply
-using CfgChf3 = Cfg3<2, 64, 16, 2, 2, 6, 2>;   // factored 3D CH (sk_chf3d.cuh)
+using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
+using CfgChf3T = Cfg3<2, 64, 32, 2, 2, 8, 1>;  // factored 3D CH, TMA loads from ghost-padded fields
 
 // Load cursor: walks the block's segment/plane sequence S-1 planes ahead of
 // the compute loop. The per-segment setup (64-bit divisions, wrapped source

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("case")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=2, help="CH steps per timed call (>= 100: graph chunks)")
     args = ap.parse_args()
     lib = _lib.ensure_device(0)
     rng = np.random.default_rng(0)
@@ -63,7 +64,7 @@ def main():
         st = CahnHilliardExplicit(g, p)
         c = DeviceArray.from_host(0.05 * rng.uniform(-1, 1, g.unknown_count()))
         s = DeviceArray(g.unknown_count())
-        ms = timer(lib, lambda: st.run_device(c, s, dt, 2), args.reps) / 2
+        ms = timer(lib, lambda: st.run_device(c, s, dt, args.steps), args.reps) / args.steps
         byts = 16.0 * g.unknown_count()
     elif case.startswith("apply"):
         dim = 2 if case == "apply2d" else 3
