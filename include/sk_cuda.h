@@ -185,6 +185,29 @@ int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk
 int sk_free_energy(const sk_grid_desc* g, const sk_ch_params* p, const double* c_dev,
                    double* energy_host, void* stream);
 
+/* ---- IMEX Cahn-Hilliard stepper (cahn_hilliard.cpp:121-189) -------------
+ * The reference's own CH path on the device: L = laplacian(d,2) and
+ * B = compose(L,L) assembled on the GPU; per step chem = L f'(c), then
+ * (I + dt M kappa B) c' = c + dt M chem (order 1) or the Crank-Nicolson /
+ * Adams-Bashforth-2 system (order 2, bootstrapped by an order-1 step and
+ * re-bootstrapped when dt changes), solved by sk_cg_solve from x0 = 0.
+ * opts NULL: the stepper's default SolveOptions{rel_tol = 1e-12}. The stepper
+ * keeps the AB2 history (prev_explicit_) and the cached implicit matrix
+ * (ensure_implicit_matrix) between calls, like CahnHilliardStepper. */
+typedef struct sk_ch_imex sk_ch_imex;
+int sk_ch_imex_create(const sk_grid_desc* g, const sk_ch_params* p, const sk_solve_options* opts,
+                      sk_ch_imex** out);
+int sk_ch_imex_destroy(sk_ch_imex* s);
+int sk_ch_imex_reset_history(sk_ch_imex* s);
+/* nsteps IMEX steps of c_dev in place; last: report of the last CG solve,
+ * cg_iterations: total CG iterations (both may be NULL). */
+int sk_ch_imex_step(sk_ch_imex* s, double* c_dev, double dt, int order, int64_t nsteps,
+                    sk_solve_report* last, int64_t* cg_iterations, void* stream);
+/* which: 0 L, 1 B, 2 the current implicit matrix identity_plus_scaled(B, factor) */
+int sk_ch_imex_matrix(const sk_ch_imex* s, int which, const sk_csr** out);
+/* ch_init (cahn_hilliard.cpp:20-63) on the host, bit-identical (origin 0). */
+int sk_ch_init_host(const sk_grid_desc* g, double c0, double eps_ic, double* c_host);
+
 /* ---- CSR assembly (grid.cpp:62-158) and SpMV (kernels.cpp:8-17) --------- */
 int sk_csr_assemble(const sk_stencil* s, const sk_grid_desc* g, int index_bits, sk_csr** out,
                     void* stream);

@@ -75,6 +75,10 @@ class Oracle:
         L.sko_cg_solve.argtypes = [C.POINTER(SkoCsr), vp, vp, dbl, i64, C.c_int, C.POINTER(i64), C.POINTER(dbl)]
         L.sko_apply_direct.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, dbl, vp, vp, vp]
         L.sko_ch_explicit.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, vp]
+        L.sko_ch_imex.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int, i64, vp]
+        L.sko_ch_init.argtypes = [C.c_int, i64, dbl, dbl, dbl, vp]
+        L.sko_ch_imex_seq.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int, vp, vp, vp, vp]
+        L.sko_identity_plus_scaled.argtypes = [C.POINTER(SkoCsr), dbl, C.POINTER(SkoCsr)]
         L.sko_free_energy.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, vp]
         L.sko_free_energy.restype = dbl
         L.sko_biharmonic_clamped.argtypes = [C.c_int, i64, vp, vp]
@@ -157,6 +161,50 @@ class Oracle:
         if st:
             raise ValueError(f"oracle ch_explicit failed with status {st}")
         return c
+
+    def ch_imex(self, dim, n, h, params, dt, order, nsteps, c, rel_tol=1e-12) -> np.ndarray:
+        """IMEX steps from a fresh stepper (cahn_hilliard.cpp:121-189), serial CG."""
+        c = np.ascontiguousarray(c, np.float64).ravel().copy()
+        st = self.L.sko_ch_imex(dim, n, h, params.mobility, params.kappa, params.rho_w, params.c_alpha,
+                                params.c_beta, rel_tol, dt, order, nsteps, _p(c))
+        if st:
+            raise ValueError(f"oracle ch_imex failed with status {st}")
+        return c
+
+    def ch_imex_seq(self, dim, n, h, params, seq, c, rel_tol=1e-12) -> np.ndarray:
+        """IMEX legs [(dt, order, steps), ...] on one fresh stepper (AB2 history across legs)."""
+        c = np.ascontiguousarray(c, np.float64).ravel().copy()
+        dts = np.ascontiguousarray([float(s[0]) for s in seq], np.float64)
+        orders = np.ascontiguousarray([int(s[1]) for s in seq], np.int32)
+        steps = np.ascontiguousarray([int(s[2]) for s in seq], np.int64)
+        st = self.L.sko_ch_imex_seq(dim, n, h, params.mobility, params.kappa, params.rho_w, params.c_alpha,
+                                    params.c_beta, rel_tol, len(seq), _p(dts), _p(orders), _p(steps), _p(c))
+        if st:
+            raise ValueError(f"oracle ch_imex_seq failed with status {st}")
+        return c
+
+    def ch_init(self, dim, n, h, c0, eps) -> np.ndarray:
+        out = np.empty(n ** dim)
+        self.L.sko_ch_init(dim, n, h, c0, eps, _p(out))
+        return out
+
+    def identity_plus_scaled(self, rp, ci, vals, alpha):
+        m, out = SkoCsr(), SkoCsr()
+        rp = np.ascontiguousarray(rp, np.int64)
+        ci = np.ascontiguousarray(ci, np.int64)
+        vals = np.ascontiguousarray(vals, np.float64)
+        m.rows = m.cols = rp.size - 1
+        m.nnz = ci.size
+        m.row_ptr = rp.ctypes.data_as(C.POINTER(C.c_int64))
+        m.col_idx = ci.ctypes.data_as(C.POINTER(C.c_int64))
+        m.values = vals.ctypes.data_as(C.POINTER(C.c_double))
+        if self.L.sko_identity_plus_scaled(C.byref(m), alpha, C.byref(out)):
+            raise MemoryError("identity_plus_scaled")
+        r = np.ctypeslib.as_array(out.row_ptr, shape=(out.rows + 1,)).copy()
+        c = np.ctypeslib.as_array(out.col_idx, shape=(max(out.nnz, 1),))[: out.nnz].copy()
+        v = np.ctypeslib.as_array(out.values, shape=(max(out.nnz, 1),))[: out.nnz].copy()
+        self.L.sko_csr_free(C.byref(out))
+        return r, c, v
 
     def free_energy(self, dim, n, h, params, c) -> float:
         c = np.ascontiguousarray(c, np.float64).ravel()
@@ -257,6 +305,12 @@ class Reference:
         L.skref_fit_loglog.argtypes = [C.c_int, vp, vp, C.POINTER(dbl), C.POINTER(dbl), C.POINTER(dbl)]
         L.skref_biharmonic_solve.argtypes = [C.c_int, vp, dbl, C.POINTER(dbl), C.POINTER(dbl), vp]
         L.skref_set_threads.argtypes = [C.c_int]
+        L.skref_imex_create.argtypes = [C.c_int, C.c_int, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.POINTER(vp)]
+        L.skref_imex_steps.argtypes = [vp, dbl, C.c_int, C.c_longlong, vp]
+        L.skref_imex_free.argtypes = [vp]
+        L.skref_ch_init.argtypes = [C.c_int, C.c_int, dbl, dbl, dbl, vp]
+        L.skref_identity_plus_scaled.argtypes = [vp, dbl]
+        L.skref_identity_plus_scaled.restype = vp
         self.L = L
 
     def err(self) -> str:
@@ -331,6 +385,27 @@ class Reference:
     def ch_free(self, handle) -> None:
         self.L.skref_ch_free(handle)
 
+    def imex_create(self, dim, n, h, params, rel_tol=1e-12):
+        out = vp()
+        st = self.L.skref_imex_create(dim, n, h, params.mobility, params.kappa, params.rho_w, params.c_alpha,
+                                      params.c_beta, rel_tol, C.byref(out))
+        if st:
+            raise RuntimeError(self.err())
+        return out
+
+    def imex_steps(self, handle, dt, order, nsteps, c: np.ndarray) -> None:
+        if self.L.skref_imex_steps(handle, dt, order, nsteps, _p(c)):
+            raise RuntimeError(self.err())
+
+    def imex_free(self, handle) -> None:
+        self.L.skref_imex_free(handle)
+
+    def ch_init(self, dim, n, h, c0, eps) -> np.ndarray:
+        out = np.empty(n ** dim)
+        if self.L.skref_ch_init(dim, n, h, c0, eps, _p(out)):
+            raise RuntimeError(self.err())
+        return out
+
     def free_energy(self, dim, n, h, params, c, serial=False) -> float:
         c = np.ascontiguousarray(c, np.float64)
         return self.L.skref_free_energy(dim, n, h, params.kappa, params.rho_w, params.c_alpha, params.c_beta, _p(c),
@@ -351,6 +426,13 @@ class RefCsr:
         self.h = out
         self.rows = ref.L.skref_csr_rows(out)
         self.nnz = ref.L.skref_csr_nnz(out)
+
+    def arrays(self):
+        rp = np.empty(self.rows + 1, np.int64)
+        ci = np.empty(max(self.nnz, 1), np.int64)
+        v = np.empty(max(self.nnz, 1))
+        self.ref.L.skref_csr_copy(self.h, _p(rp), _p(ci), _p(v))
+        return rp, ci[: self.nnz], v[: self.nnz]
 
     def matvec(self, x: np.ndarray, y: np.ndarray, serial: bool = False) -> None:
         self.ref.L.skref_csr_matvec(self.h, _p(x), _p(y), int(serial))

@@ -373,6 +373,68 @@ void skref_ch_steps(void* sp, double dt, long long nsteps, double* c) {
 
 void skref_ch_free(void* s) { delete static_cast<ChExplicit*>(s); }
 
+// The reference IMEX stepper itself (cahn_hilliard.cpp:121-189): one
+// CahnHilliardStepper per handle, so the AB2 history and the implicit-matrix
+// cache persist across calls exactly as in the reference.
+struct ImexHandle {
+  GridSpec grid;
+  CahnHilliardStepper stepper;
+  ImexHandle(const GridSpec& g, const CahnHilliardParams& p, double rel_tol)
+      : grid(g), stepper(g, p, SolveOptions{.rel_tol = rel_tol}) {}
+};
+
+int skref_imex_create(int dim, int n, double h, double mobility, double kappa, double rho_w,
+                      double c_alpha, double c_beta, double rel_tol, void** out) {
+  try {
+    GridSpec g = make_periodic_grid(dim, n, h);
+    *out = new ImexHandle(g, ch_params(mobility, kappa, rho_w, c_alpha, c_beta), rel_tol);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail_std(e);
+  }
+}
+
+int skref_imex_steps(void* hp, double dt, int order, long long nsteps, double* c) {
+  try {
+    auto* hd = static_cast<ImexHandle*>(hp);
+    CahnHilliardState st;
+    st.grid = hd->grid;
+    st.c.assign(c, c + hd->grid.unknown_count());
+    for (long long k = 0; k < nsteps; ++k) hd->stepper.step(st, dt, order);
+    std::memcpy(c, st.c.data(), st.c.size() * sizeof(double));
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail_std(e);
+  }
+}
+
+void skref_imex_free(void* h) { delete static_cast<ImexHandle*>(h); }
+
+// ch_init (cahn_hilliard.cpp:20-63) with the given c0 / eps_ic
+int skref_ch_init(int dim, int n, double h, double c0, double eps_ic, double* out) {
+  try {
+    CahnHilliardParams p;
+    p.c0 = c0;
+    p.eps_ic = eps_ic;
+    CahnHilliardState st = ch_init(make_periodic_grid(dim, n, h), p);
+    std::memcpy(out, st.c.data(), st.c.size() * sizeof(double));
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail_std(e);
+  }
+}
+
+// identity_plus_scaled (linalg.cpp:224-251) on an assembled operator
+void* skref_identity_plus_scaled(void* mp, double alpha) {
+  return new CsrMatrix(identity_plus_scaled(*static_cast<CsrMatrix*>(mp), alpha));
+}
+
 double skref_free_energy(int dim, int n, double h, double kappa, double rho_w, double c_alpha,
                          double c_beta, const double* c, int serial) {
   CahnHilliardState st;

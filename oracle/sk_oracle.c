@@ -433,6 +433,161 @@ int sko_ch_explicit(int dim, int64_t n, double h, double mobility, double kappa,
   return 0;
 }
 
+/* identity_plus_scaled (linalg.cpp:224-251): v = alpha b (+1 on the diagonal),
+ * exact zeros dropped, a missing diagonal inserted as 1.0, columns sorted. */
+int sko_identity_plus_scaled(const sko_csr* m, double alpha, sko_csr* out) {
+  const int64_t rows = m->rows;
+  out->rows = rows;
+  out->cols = m->cols;
+  out->row_ptr = (int64_t*)calloc((size_t)rows + 1, sizeof(int64_t));
+  out->col_idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m->nnz + rows + 1));
+  out->values = (double*)malloc(sizeof(double) * (size_t)(m->nnz + rows + 1));
+  if (!out->row_ptr || !out->col_idx || !out->values) return 1;
+  int64_t o = 0;
+  for (int64_t i = 0; i < rows; ++i) {
+    int diag = 0, placed = 0;
+    for (int64_t k = m->row_ptr[i]; k < m->row_ptr[i + 1]; ++k) {
+      const int64_t j = m->col_idx[k];
+      if (!placed && j > i) { /* the sorted position of an inserted diagonal */
+        if (!diag) {
+          out->col_idx[o] = i;
+          out->values[o++] = 1.0;
+        }
+        placed = 1;
+      }
+      double v = alpha * m->values[k];
+      if (j == i) {
+        v += 1.0;
+        diag = placed = 1;
+      }
+      if (v != 0.0) {
+        out->col_idx[o] = j;
+        out->values[o++] = v;
+      }
+    }
+    if (!diag && !placed) {
+      out->col_idx[o] = i;
+      out->values[o++] = 1.0;
+    }
+    out->row_ptr[i + 1] = o;
+  }
+  out->nnz = o;
+  return 0;
+}
+
+/* IMEX stepping (cahn_hilliard.cpp:121-189) on ONE fresh stepper over a
+ * sequence of legs (dt, order, steps): L, B assembled (:126-128); per step
+ * chem = L f'(c) (:146-152); AB2 only with a same-dt history (:155-157),
+ * the history kept by order-2 steps and dropped by order-1 steps (:183-188);
+ * implicit matrix per (factor, order) (:131-137); rhs (:159-178);
+ * c = cg_solve(implicit, rhs, rel_tol) from x0 = 0 (:180). */
+int sko_ch_imex_seq(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
+                    double c_beta, double rel_tol, int nlegs, const double* dts, const int* orders,
+                    const int64_t* steps, double* c) {
+  int lo[3 * 7], bo[3 * 49];
+  double lc[7], bcf[49];
+  const int nl = lap_entries(dim, lo, lc);
+  const int nb = compose_entries(dim, nl, lo, lc, bo, bcf);
+  const int64_t nn[3] = {n, n, n};
+  const int bcs[3] = {0, 0, 0};
+  sko_csr L, B, A;
+  int st = sko_assemble(dim, nl, lo, lc, -2, nn, h, bcs, &L);
+  if (st) return st;
+  st = sko_assemble(dim, nb, bo, bcf, -4, nn, h, bcs, &B);
+  if (st) {
+    sko_csr_free(&L);
+    return st;
+  }
+  const int64_t rows = L.rows;
+  double* w = (double*)malloc(sizeof(double) * (size_t)rows);
+  double* chem = (double*)malloc(sizeof(double) * (size_t)rows);
+  double* prev = (double*)malloc(sizeof(double) * (size_t)rows);
+  double* rhs = (double*)malloc(sizeof(double) * (size_t)rows);
+  double* bc = (double*)malloc(sizeof(double) * (size_t)rows);
+  int have_prev = 0, a_order = 0;
+  double a_factor = 0.0, prev_dt = 0.0;
+  A.row_ptr = NULL;
+  for (int leg = 0; leg < nlegs && st == 0; ++leg) {
+    const double dt = dts[leg];
+    const int order = orders[leg];
+    for (int64_t k = 0; k < steps[leg] && st == 0; ++k) {
+      for (int64_t i = 0; i < rows; ++i) w[i] = f_chem_prime(c[i], rho_w, c_alpha, c_beta);
+      sko_csr_matvec(&L, w, chem);
+      const int eff = (order == 2 && have_prev && prev_dt == dt) ? 2 : 1;
+      const double factor = dt * mobility * kappa * (eff == 2 ? 0.5 : 1.0);
+      if (!A.row_ptr || factor != a_factor || eff != a_order) {
+        if (A.row_ptr) sko_csr_free(&A);
+        sko_identity_plus_scaled(&B, factor, &A);
+        a_factor = factor;
+        a_order = eff;
+      }
+      if (eff == 1) {
+        for (int64_t i = 0; i < rows; ++i) rhs[i] = c[i] + dt * mobility * chem[i];
+      } else {
+        sko_csr_matvec(&B, c, bc);
+        const double half = 0.5 * dt * mobility * kappa;
+        for (int64_t i = 0; i < rows; ++i)
+          rhs[i] = c[i] - half * bc[i] + dt * mobility * (1.5 * chem[i] - 0.5 * prev[i]);
+      }
+      int64_t it = 0;
+      double res = 0;
+      st = sko_cg_solve(&A, rhs, c, rel_tol, 0, 0, &it, &res);
+      if (order == 2) {
+        double* t = prev;
+        prev = chem;
+        chem = t;
+        have_prev = 1;
+        prev_dt = dt;
+      } else {
+        have_prev = 0;
+      }
+    }
+  }
+  if (A.row_ptr) sko_csr_free(&A);
+  free(w);
+  free(chem);
+  free(prev);
+  free(rhs);
+  free(bc);
+  sko_csr_free(&L);
+  sko_csr_free(&B);
+  return st;
+}
+
+int sko_ch_imex(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
+                double c_beta, double rel_tol, double dt, int order, int64_t nsteps, double* c) {
+  return sko_ch_imex_seq(dim, n, h, mobility, kappa, rho_w, c_alpha, c_beta, rel_tol, 1, &dt, &order, &nsteps, c);
+}
+
+/* ch_init (cahn_hilliard.cpp:20-63), origin 0 */
+void sko_ch_init(int dim, int64_t n, double h, double c0, double eps, double* out) {
+  if (dim == 2) {
+    for (int64_t j = 0; j < n; ++j) {
+      const double y = 0.0 + (int)j * h;
+      for (int64_t i = 0; i < n; ++i) {
+        const double x = 0.0 + (int)i * h;
+        const double c2 = cos(0.13 * x) * cos(0.087 * y);
+        out[j * n + i] = c0 + eps * (cos(0.105 * x) * cos(0.11 * y) + c2 * c2 +
+                                     cos(0.025 * x - 0.15 * y) * cos(0.07 * x - 0.02 * y));
+      }
+    }
+  } else {
+    for (int64_t k = 0; k < n; ++k) {
+      const double z = 0.0 + (int)k * h;
+      for (int64_t j = 0; j < n; ++j) {
+        const double y = 0.0 + (int)j * h;
+        for (int64_t i = 0; i < n; ++i) {
+          const double x = 0.0 + (int)i * h;
+          const double c2 = cos(0.13 * x) * cos(0.087 * y) * cos(0.1 * z);
+          out[(k * n + j) * n + i] =
+              c0 + eps * (cos(0.105 * x) * cos(0.11 * y) * cos(0.11 * z) + c2 * c2 +
+                          cos(0.025 * x - 0.15 * y - 0.1 * z) * cos(0.07 * x - 0.02 * y + 0.01 * z));
+        }
+      }
+    }
+  }
+}
+
 /* free_energy, serial form (cahn_hilliard.cpp:77-107,116-119) */
 double sko_free_energy(int dim, int64_t n, double h, double kappa, double rho_w, double c_alpha, double c_beta,
                        const double* c) {

@@ -38,6 +38,13 @@ void sko_apply_direct(int dim, int nent, const int* off, const double* coeff, in
                       const int* bc, const double* u, double* v);
 int sko_ch_explicit(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
                     double c_beta, double dt, int64_t nsteps, double* c);
+int sko_identity_plus_scaled(const sko_csr* m, double alpha, sko_csr* out);
+int sko_ch_imex_seq(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
+                    double c_beta, double rel_tol, int nlegs, const double* dts, const int* orders,
+                    const int64_t* steps, double* c);
+int sko_ch_imex(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
+                double c_beta, double rel_tol, double dt, int order, int64_t nsteps, double* c);
+void sko_ch_init(int dim, int64_t n, double h, double c0, double eps, double* out);
 double sko_free_energy(int dim, int64_t n, double h, double kappa, double rho_w, double c_alpha, double c_beta,
                        const double* c);
 void sko_biharmonic_clamped(int dim, int64_t intervals, double* f, double* u_exact);

@@ -73,6 +73,13 @@ SIGNATURES = {
                                C.POINTER(c_int), vp]),
     "sk_ch_explicit_host": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, c_i64, vp]),
     "sk_free_energy": (c_int, [C.POINTER(GridDesc), C.POINTER(ChParams), vp, pd, vp]),
+    "sk_ch_imex_create": (c_int, [C.POINTER(GridDesc), C.POINTER(ChParams), C.POINTER(SolveOptionsC),
+                                  C.POINTER(vp)]),
+    "sk_ch_imex_destroy": (c_int, [vp]),
+    "sk_ch_imex_reset_history": (c_int, [vp]),
+    "sk_ch_imex_step": (c_int, [vp, vp, c_dbl, c_int, c_i64, C.POINTER(SolveReportC), C.POINTER(c_i64), vp]),
+    "sk_ch_imex_matrix": (c_int, [vp, c_int, C.POINTER(vp)]),
+    "sk_ch_init_host": (c_int, [C.POINTER(GridDesc), c_dbl, c_dbl, vp]),
     "sk_csr_assemble": (c_int, [vp, C.POINTER(GridDesc), c_int, C.POINTER(vp), vp]),
     "sk_csr_upload": (c_int, [c_i64, c_i64, c_i64, vp, vp, vp, c_int, C.POINTER(vp)]),
     "sk_csr_info": (c_int, [vp, C.POINTER(c_i64), C.POINTER(c_i64), C.POINTER(c_i64), C.POINTER(c_int)]),

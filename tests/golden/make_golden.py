@@ -99,6 +99,23 @@ def main() -> None:
                             meta=np.array([dim, n, steps, seed], np.int64), params=np.array([eps * eps, 1.0, 0.25, -1.0, 1.0]),
                             energy0=np.float64(e0), energy=np.float64(e1))
 
+    # the reference's IMEX stepper (cahn_hilliard.cpp:121-189) with its benchmark
+    # parameters, from ch_init (:20-63); "seq" = (dt, order, steps) legs on ONE
+    # stepper, so the AB2 history and its re-bootstrap on a dt change are pinned
+    pd = P(2.0, 5.0, 5.0, 0.3, 0.7)
+    for name, dim, n, h, seq in [("imex_2d_o1", 2, 24, 1.0, [(0.05, 1, 5)]),
+                                 ("imex_2d_o2", 2, 24, 1.0, [(0.05, 2, 6)]),
+                                 ("imex_3d_o2", 3, 10, 1.0, [(0.05, 2, 4)]),
+                                 ("imex_2d_dtchange", 2, 20, 0.5, [(0.02, 2, 3), (0.01, 2, 3), (0.01, 1, 1), (0.01, 2, 2)])]:
+        c0 = ref.ch_init(dim, n, h, 0.5, 0.01)
+        c = c0.copy()
+        hd = ref.imex_create(dim, n, h, pd, 1e-12)
+        for dt, order, steps in seq:
+            ref.imex_steps(hd, dt, order, steps, c)
+        ref.imex_free(hd)
+        np.savez_compressed(OUT / f"{name}.npz", c0=c0, c=c, h=np.float64(h), meta=np.array([dim, n], np.int64),
+                            seq=np.array(seq, np.float64), params=np.array([2.0, 5.0, 5.0, 0.3, 0.7]))
+
     # the reference's benchmark chemistry (cahn_hilliard.hpp:14-22) on a few values
     cs = np.linspace(-1.5, 1.5, 31)
     fp = np.array([ref.L.skref_f_chem_prime(float(x), 5.0, 0.3, 0.7) for x in cs])

@@ -236,3 +236,44 @@ def test_oracle_vs_reference_config_sizes(orc, ref):
         got = orc.assemble(s, g)
         want = ref.assemble(dim, acc, 2, [n] * dim, h, [bc] * dim)
         assert all(np.array_equal(a, b) for a, b in zip(got, want))
+
+
+# ------------------------------------------------------------- IMEX (§8f 1) --
+@pytest.mark.parametrize("path", sorted(GOLD.glob("imex_*.npz")), ids=lambda p: p.stem)
+def test_oracle_imex_bit_exact(orc, path):
+    # the C restatement of CahnHilliardStepper::step (order 1, order 2, and the
+    # AB2 re-bootstrap on a dt change) reproduces the reference run bit for bit
+    from paper_2205_03354_b200.cahn_hilliard import CahnHilliardParams
+
+    d = np.load(path)
+    dim, n = (int(x) for x in d["meta"])
+    h = float(d["h"])
+    assert np.array_equal(orc.ch_init(dim, n, h, 0.5, 0.01), d["c0"])
+    seq = [(float(a), int(b), int(c)) for a, b, c in d["seq"]]
+    c = orc.ch_imex_seq(dim, n, h, CahnHilliardParams(), seq, d["c0"])
+    assert np.array_equal(c, d["c"])
+
+
+def test_oracle_identity_plus_scaled_vs_reference(orc, ref):
+    # linalg.cpp:224-251 on assembled operators, incl. a missing diagonal
+    from oracle.ffi import RefCsr
+
+    for dim, acc, n in [(2, 2, 9), (3, 2, 5)]:
+        m = RefCsr(ref, dim, acc, 2, [n] * dim, 1.0, [0] * dim)  # bilaplacian, periodic
+        rp, ci, v = m.arrays()
+        for alpha in (0.37, -1.0 / v[0] if v[0] else 1.0):
+            out = ref.L.skref_identity_plus_scaled(m.h, alpha)
+            rows, nnz = ref.L.skref_csr_rows(out), ref.L.skref_csr_nnz(out)
+            r2, c2, v2 = np.empty(rows + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+            ref.L.skref_csr_copy(out, r2.ctypes.data, c2.ctypes.data, v2.ctypes.data)
+            ref.L.skref_csr_free(out)
+            r1, c1, v1 = orc.identity_plus_scaled(rp, ci, v, alpha)
+            assert np.array_equal(r1, r2) and np.array_equal(c1, c2) and np.array_equal(v1, v2)
+    # a matrix without diagonal entries: the reference inserts 1.0 in sorted position
+    rp = np.array([0, 2, 3, 4], np.int64)
+    ci = np.array([1, 2, 0, 1], np.int64)
+    v = np.array([1.0, 2.0, 3.0, 4.0])
+    r, c, vals = orc.identity_plus_scaled(rp, ci, v, 0.5)
+    assert r.tolist() == [0, 3, 5, 7]
+    assert c.tolist() == [0, 1, 2, 0, 1, 1, 2]
+    assert vals.tolist() == [1.0, 0.5, 1.0, 1.5, 1.0, 2.0, 1.0]
