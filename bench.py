@@ -379,6 +379,48 @@ def extra_cg(lib, N: int = 1024, iters: int = 256):
             "ms_per_iteration": per, "achieved_gbs": bytes_it / (per * 1e-3) / 1e9}
 
 
+def extra_imex(lib, dim: int = 2, n: int = 1024, steps: int = 10, ref_steps: int = 2):
+    """The reference's own CH path (IMEX, CahnHilliardStepper, order 2 = CN/AB2) on
+    the device vs the compiled reference on the host cores; reference benchmark
+    parameters, ch_init field, dt = 0.05, h = 1."""
+    from paper_2205_03354_b200.cahn_hilliard import CahnHilliardParams, CahnHilliardStepper, ch_init
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.grid import make_periodic_grid
+
+    p = CahnHilliardParams()
+    g = make_periodic_grid(dim, n, 1.0)
+    c0 = ch_init(g).c
+    st = CahnHilliardStepper(g, p)
+    c = DeviceArray.from_host(c0)
+    st.step_device(c, 0.05, 2, 2)  # bootstrap + both implicit matrices (not timed)
+    ev = Events(lib)
+    its = 0
+    ev.start()
+    for _ in range(steps):
+        st.step_device(c, 0.05, 2, 1)
+        its += st.last_cg_iterations
+    ms = ev.stop_ms() / steps
+    out = {"config": f"IMEX CH (reference CahnHilliardStepper, order 2) {n}^{dim}, dt 0.05",
+           "value": 1e3 / ms, "unit": "steps/s", "ms_per_step": ms, "cg_iterations_per_step": its / steps,
+           "note": "matrix-free implicit operator in a device-side CG while loop"}
+    try:
+        from oracle.ffi import Reference
+
+        ref = Reference()
+        hd = ref.imex_create(dim, n, 1.0, p)
+        cr = c0.copy()
+        ref.imex_steps(hd, 0.05, 2, 2, cr)
+        t0 = time.perf_counter()
+        ref.imex_steps(hd, 0.05, 2, ref_steps, cr)
+        el = (time.perf_counter() - t0) / ref_steps
+        ref.imex_free(hd)
+        out["reference_cpu"] = {"ms_per_step": el * 1e3, "cores": ref.threads(),
+                                "sample": f"{ref_steps} order-2 steps after a 2-step bootstrap"}
+    except Exception as ex:  # the reference library only exists where it was built
+        out["reference_cpu"] = {"unavailable": repr(ex)}
+    return out
+
+
 # ----------------------------------------------------------- CPU reference --
 def ref_ch_steps_per_s(dim: int, steps: int, warmup: int):
     """The reference library on the host cores: restated explicit CH step."""
@@ -481,7 +523,8 @@ def main() -> int:
         for fn in (lambda: extra_apply2d(lib), lambda: run_ch_2d_extra(lib, dim, args),
                    lambda: run_ch_2d_extra(lib, dim, args, "composed", same=True),
                    lambda: extra_apply3d(lib, "25"), lambda: extra_apply3d(lib, "73"),
-                   lambda: extra_csr73(lib, 64), lambda: extra_csr73(lib, 32), lambda: extra_cg(lib)):
+                   lambda: extra_csr73(lib, 64), lambda: extra_csr73(lib, 32), lambda: extra_cg(lib),
+                   lambda: extra_imex(lib, 2, 1024), lambda: extra_imex(lib, 3, 128, ref_steps=1)):
             try:
                 e = fn()
                 if e:

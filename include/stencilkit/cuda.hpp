@@ -277,4 +277,57 @@ inline double free_energy(const CahnHilliardState& s, const CahnHilliardParams& 
 }
 }  // namespace stencilkit::cuda
 
+namespace stencilkit::cuda {
+/// IMEX stepper (cahn_hilliard.hpp:47-68 / cahn_hilliard.cpp:121-189) on the
+/// device: same constructor arguments and step(state, dt, order) contract
+/// (AB2 history and implicit-matrix cache kept between calls; errors thrown
+/// as stencilkit::Error). The field is copied in and out per call; use
+/// step_device for a device-resident field.
+class CahnHilliardStepper {
+ public:
+  CahnHilliardStepper(const GridSpec& grid, const CahnHilliardParams& p, SolveOptions solve = {.rel_tol = 1e-12})
+      : grid_(grid), desc_(grid_desc(grid)), params_(ch_params(p)) {
+    const sk_solve_options o{solve.rel_tol, solve.max_iter, solve.deflate_mean ? 1 : 0, 0, 0, 0};
+    sk_ch_imex* h = nullptr;
+    check(sk_ch_imex_create(&desc_, &params_, &o, &h));
+    h_.reset(h);
+  }
+  void step(CahnHilliardState& s, double dt, int order) {
+    if (static_cast<int64_t>(s.c.size()) != grid_.unknown_count())
+      throw Error(Errc::shape_mismatch, "state does not match the stepper grid");
+    DeviceField c(s.c);
+    check(sk_ch_imex_step(h_.get(), c.data(), dt, order, 1, nullptr, nullptr, nullptr));
+    c.download(s.c);
+    s.t += dt;
+  }
+  /// nsteps steps of a device-resident field (caller-owned device pointer)
+  void step_device(double* c_dev, double dt, int order, std::int64_t nsteps = 1, void* stream = nullptr) {
+    check(sk_ch_imex_step(h_.get(), c_dev, dt, order, nsteps, nullptr, nullptr, stream));
+  }
+
+ private:
+  struct Del {
+    void operator()(sk_ch_imex* h) const { sk_ch_imex_destroy(h); }
+  };
+  GridSpec grid_;
+  sk_grid_desc desc_;
+  sk_ch_params params_;
+  std::unique_ptr<sk_ch_imex, Del> h_;
+};
+
+inline void imex_step(CahnHilliardStepper& stepper, CahnHilliardState& s, double dt, int order) {
+  stepper.step(s, dt, order);
+}
+
+/// ch_init (cahn_hilliard.cpp:20-63), bit-identical (origin 0 grids).
+inline CahnHilliardState ch_init(const GridSpec& grid, const CahnHilliardParams& p) {
+  CahnHilliardState s;
+  s.grid = grid;
+  s.c.resize(static_cast<size_t>(grid.unknown_count()));
+  const sk_grid_desc d = grid_desc(grid);
+  check(sk_ch_init_host(&d, p.c0, p.eps_ic, s.c.data()));
+  return s;
+}
+}  // namespace stencilkit::cuda
+
 #endif  // STENCILKIT_CUDA_HPP

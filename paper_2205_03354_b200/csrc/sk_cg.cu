@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "sk_internal.hpp"
@@ -99,7 +100,14 @@ __global__ void __launch_bounds__(kT) k2_update_rr(int64_t n, const double* __re
   }
 }
 
-__global__ void k3_xpby(int64_t n, const double* __restrict__ r, double* __restrict__ p, const CgState* st) {
+// COND: the body of a device-side while loop (conditional graph node): the
+// first thread publishes "keep iterating" for the next round.
+template <bool COND>
+__global__ void k3_xpby(int64_t n, const double* __restrict__ r, double* __restrict__ p, const CgState* st,
+                        cudaGraphConditionalHandle cond) {
+  if constexpr (COND) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, st->status == kRunning ? 1u : 0u);
+  }
   if (st->status != kRunning) return;
   const double beta = st->beta;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
@@ -172,86 +180,240 @@ __global__ void k_shift(int64_t n, double* __restrict__ x, double mean) {
     x[i] -= mean;
 }
 
-struct Solver {
-  const sk_csr* m;
-  cudaStream_t stream;
-  int64_t n;
-  int grid;
+// matrix-free operator: K1 split into the stencil apply q = A p and this p.q pass
+__global__ void __launch_bounds__(kT) k_pq(int64_t n, const double* __restrict__ p, const double* __restrict__ q,
+                                           CgState* st, double* partials) {
+  if (st->status != kRunning) return;
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT)
+    acc = fma(p[i], q[i], acc);
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[0])) {
+    const double pq = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->pq = pq;
+      if (pq <= 0) st->status = kNotPD;
+      else st->alpha = st->rho / pq;
+    }
+  }
+}
+
+// sum (b - q)^2 with q = A x already applied (matrix-free true residual)
+__global__ void __launch_bounds__(kT) k_resid(int64_t n, const double* __restrict__ b, const double* __restrict__ q,
+                                              CgState* st, double* partials) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    const double d = __dsub_rn(b[i], q[i]);
+    acc = fma(d, d, acc);
+  }
+  acc = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (last_block(&st->counter[2])) {
+    const double t = reduce_partials<kT>(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) st->scalar_out = t;
+  }
+}
+
+}  // namespace
+
+// A CG workspace (r, p, q, partials, device state) plus the captured graph of
+// `check_every` iterations for one solution pointer x. Reused across solves
+// (the IMEX stepper solves one system per time step).
+struct CgPlan {
+  CgOperator op;
+  int64_t n = 0;
+  int grid = 0;
+  int check_every = 64;
+  char* ws = nullptr;
   CgState* st = nullptr;  // device
   double* partials = nullptr;
   double *r = nullptr, *p = nullptr, *q = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const double* graph_x = nullptr;
+  bool device_loop = false;  // exec = while(status == running) { iteration } on the device
+  int kernels_per_iteration() const { return op.m ? 3 : 4; }
 
-  int launch_k1() {
-    if (m->index_bits == 32)
-      k1_spmv_pq<int32_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len, static_cast<const int32_t*>(m->sell_col),
-                                                    m->sell_val, p, q, st, partials);
-    else
-      k1_spmv_pq<int64_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len, static_cast<const int64_t*>(m->sell_col),
-                                                    m->sell_val, p, q, st, partials);
-    SK_LAUNCH_CHECK("k1_spmv_pq");
+  ~CgPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (ws) cudaFree(ws);
+  }
+
+  // q = A p (+ p.q, alpha)
+  int launch_q(cudaStream_t stream) {
+    if (op.m) {
+      const sk_csr* m = op.m;
+      if (m->index_bits == 32)
+        k1_spmv_pq<int32_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
+                                                      static_cast<const int32_t*>(m->sell_col), m->sell_val, p, q,
+                                                      st, partials);
+      else
+        k1_spmv_pq<int64_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
+                                                      static_cast<const int64_t*>(m->sell_col), m->sell_val, p, q,
+                                                      st, partials);
+      SK_LAUNCH_CHECK("k1_spmv_pq");
+      return SK_OK;
+    }
+    if (int e = launch_apply(op.s, op.g, p, q, stream)) return e;
+    k_pq<<<grid, kT, 0, stream>>>(n, p, q, st, partials);
+    SK_LAUNCH_CHECK("k_pq");
     return SK_OK;
   }
-  int true_residual(const double* x, const double* b, double* out) {
-    if (m->index_bits == 32)
-      k_true_residual<int32_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
-                                                         static_cast<const int32_t*>(m->sell_col), m->sell_val, x, b, q,
-                                                         st, partials);
-    else
-      k_true_residual<int64_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
-                                                         static_cast<const int64_t*>(m->sell_col), m->sell_val, x, b, q,
-                                                         st, partials);
-    SK_LAUNCH_CHECK("k_true_residual");
+  int true_residual(const double* x, const double* b, double* out, cudaStream_t stream) {
+    if (op.m) {
+      const sk_csr* m = op.m;
+      if (m->index_bits == 32)
+        k_true_residual<int32_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
+                                                           static_cast<const int32_t*>(m->sell_col), m->sell_val, x, b,
+                                                           q, st, partials);
+      else
+        k_true_residual<int64_t><<<grid, kT, 0, stream>>>(n, m->sell_ptr, m->sell_len,
+                                                           static_cast<const int64_t*>(m->sell_col), m->sell_val, x, b,
+                                                           q, st, partials);
+      SK_LAUNCH_CHECK("k_true_residual");
+    } else {
+      if (int e = launch_apply(op.s, op.g, x, q, stream)) return e;
+      k_resid<<<grid, kT, 0, stream>>>(n, b, q, st, partials);
+      SK_LAUNCH_CHECK("k_resid");
+    }
     SK_CUDA_TRY(cudaMemcpyAsync(out, &st->scalar_out, sizeof(double), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
     *out = std::sqrt(*out);
     return SK_OK;
   }
   template <int OP>
-  int reduce(const double* a, double* out) {
+  int reduce(const double* a, double* out, cudaStream_t stream) {
     k_reduce<OP><<<grid, kT, 0, stream>>>(n, a, st, partials);
     SK_LAUNCH_CHECK("k_reduce");
     SK_CUDA_TRY(cudaMemcpyAsync(out, &st->scalar_out, sizeof(double), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
     return SK_OK;
   }
+  // The iteration graph updating x: a device-side while loop over one
+  // iteration (conditional node; one launch runs until the status leaves
+  // RUNNING), or, where conditional nodes are unavailable, check_every
+  // unrolled iterations whose kernels become no-ops after convergence.
+  int ensure_graph(double* x, cudaStream_t stream) {
+    if (exec && graph_x == x) return SK_OK;
+    if (exec) {
+      cudaGraphExecDestroy(exec);
+      exec = nullptr;
+    }
+    cudaStream_t cap = stream ? stream : capture_stream();
+    const char* env = getenv("SK_CG_DEVICE_LOOP");
+    if (!(env && env[0] == '0') && build_loop_graph(x, cap) == SK_OK) {
+      device_loop = true;
+      graph_x = x;
+      return SK_OK;
+    }
+    cudaGetLastError();  // clear a failed attempt
+    device_loop = false;
+    SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    int st_ = SK_OK;
+    for (int k = 0; k < check_every && st_ == SK_OK; ++k) st_ = iteration(x, cap, false, 0);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    g_launches -= int64_t(kernels_per_iteration()) * check_every;  // capture does not execute
+    if (st_ != SK_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st_;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    graph_x = x;
+    return SK_OK;
+  }
+  int iteration(double* x, cudaStream_t cap, bool cond, cudaGraphConditionalHandle h) {
+    if (int e = launch_q(cap)) return e;
+    k2_update_rr<<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials);
+    if (cond)
+      k3_xpby<true><<<grid, kT, 0, cap>>>(n, r, p, st, h);
+    else
+      k3_xpby<false><<<grid, kT, 0, cap>>>(n, r, p, st, h);
+    return SK_OK;
+  }
+  int build_loop_graph(double* x, cudaStream_t cap) {
+    cudaGraph_t graph = nullptr;
+    if (cudaGraphCreate(&graph, 0) != cudaSuccess) return SK_ERR_CUDA;
+    struct G {
+      cudaGraph_t g;
+      ~G() { cudaGraphDestroy(g); }
+    } guard{graph};
+    cudaGraphConditionalHandle h;
+    if (cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) return SK_ERR_CUDA;
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (cudaGraphAddNode(&node, graph, nullptr, 0, &cp) != cudaSuccess) return SK_ERR_CUDA;
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if (cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess)
+      return SK_ERR_CUDA;
+    const int st_ = iteration(x, cap, true, h);
+    cudaGraph_t out = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cap, &out);
+    g_launches -= kernels_per_iteration();  // capture does not execute
+    if (st_ != SK_OK || e != cudaSuccess) return SK_ERR_CUDA;
+    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      exec = nullptr;
+      return SK_ERR_CUDA;
+    }
+    return SK_OK;
+  }
 };
 
-}  // namespace
+int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, CgPlan** out) {
+  *out = nullptr;
+  auto* pl = new CgPlan;
+  pl->op = op;
+  pl->n = op.n;
+  pl->check_every = check_every > 0 ? check_every : 64;
+  const int64_t g = (op.n + kT - 1) / kT;
+  pl->grid = int(g > int64_t(kNumSMs) * 8 ? int64_t(kNumSMs) * 8 : (g > 0 ? g : 1));
+  if (op.m) {
+    if (int e = csr_build_sell(const_cast<sk_csr*>(op.m), stream)) {  // before any graph capture
+      delete pl;
+      return e;
+    }
+  }
+  const size_t vec = sizeof(double) * size_t(op.n > 0 ? op.n : 1);
+  const size_t ws_bytes = 3 * vec + sizeof(double) * size_t(pl->grid) + sizeof(CgState) + 256;
+  if (cudaMalloc(reinterpret_cast<void**>(&pl->ws), ws_bytes) != cudaSuccess) {
+    delete pl;
+    return fail(SK_ERR_OUT_OF_MEMORY, "cg workspace");
+  }
+  pl->r = reinterpret_cast<double*>(pl->ws);
+  pl->p = pl->r + op.n;
+  pl->q = pl->p + op.n;
+  pl->partials = pl->q + op.n;
+  pl->st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(pl->partials + pl->grid) + 127) & ~uintptr_t(127));
+  *out = pl;
+  return SK_OK;
+}
 
-int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
-             cudaStream_t stream) {
-  if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
-  const int64_t n = m->rows;
+void cg_plan_destroy(CgPlan* p) { delete p; }
+
+int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
+                  cudaStream_t stream) {
+  const int64_t n = s->n;
   sk_solve_options opts{1e-10, 0, 0, 0, 0, 0};
   if (o) opts = *o;
   const int64_t max_iter = opts.max_iter > 0 ? opts.max_iter : 10 * n;  // linalg.cpp:20
-  const int check_every = opts.check_every > 0 ? opts.check_every : 64;
   sk_solve_report report{0, 0, 0.0, 0.0};
   if (rep) *rep = report;
   if (n == 0) return SK_OK;
-
-  if (int e = csr_build_sell(const_cast<sk_csr*>(m), stream)) return e;  // before any graph capture
-  Solver s{m, stream, n};
-  int64_t g = (n + kT - 1) / kT;
-  s.grid = int(g > int64_t(kNumSMs) * 8 ? int64_t(kNumSMs) * 8 : g);
   const size_t vec = sizeof(double) * size_t(n);
-  char* ws = nullptr;
-  const size_t ws_bytes = 3 * vec + sizeof(double) * size_t(s.grid) + sizeof(CgState) + 256;
-  SK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, stream));
-  struct Free {
-    char* p;
-    cudaStream_t s;
-    ~Free() { cudaFreeAsync(p, s); }
-  } guard{ws, stream};
-  s.r = reinterpret_cast<double*>(ws);
-  s.p = s.r + n;
-  s.q = s.p + n;
-  s.partials = s.q + n;
-  s.st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(s.partials + s.grid) + 127) & ~uintptr_t(127));
 
-  SK_CUDA_TRY(cudaMemsetAsync(s.st, 0, sizeof(CgState), stream));
+  SK_CUDA_TRY(cudaMemsetAsync(s->st, 0, sizeof(CgState), stream));
   double bb = 0;
-  if (int e = s.reduce<0>(b, &bb)) return e;
+  if (int e = s->reduce<0>(b, &bb, stream)) return e;
   const double bnorm = std::sqrt(bb);  // :23
   if (bnorm == 0.0) {                  // :24
     SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
@@ -261,16 +423,16 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   if (opts.use_initial_guess) {
     // extension: r = b - M x0, p = r (the restart kernel computes exactly that)
     double dummy = 0;
-    if (int e = s.true_residual(x, b, &dummy)) return e;
-    k_restart<<<s.grid, kT, 0, stream>>>(n, b, s.q, s.r, s.p, s.st, s.partials);
+    if (int e = s->true_residual(x, b, &dummy, stream)) return e;
+    k_restart<<<s->grid, kT, 0, stream>>>(n, b, s->q, s->r, s->p, s->st, s->partials);
     SK_LAUNCH_CHECK("k_restart");
-    SK_CUDA_TRY(cudaMemcpyAsync(&rho0, &s.st->rho, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    SK_CUDA_TRY(cudaMemcpyAsync(&rho0, &s->st->rho, sizeof(double), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
   } else {
     // x = 0, r = p = b (linalg.cpp:22)
     SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
-    SK_CUDA_TRY(cudaMemcpyAsync(s.r, b, vec, cudaMemcpyDeviceToDevice, stream));
-    SK_CUDA_TRY(cudaMemcpyAsync(s.p, b, vec, cudaMemcpyDeviceToDevice, stream));
+    SK_CUDA_TRY(cudaMemcpyAsync(s->r, b, vec, cudaMemcpyDeviceToDevice, stream));
+    SK_CUDA_TRY(cudaMemcpyAsync(s->p, b, vec, cudaMemcpyDeviceToDevice, stream));
   }
   const double target = opts.rel_tol * bnorm;
   CgState h{};
@@ -279,42 +441,8 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   h.it = 0;
   h.max_iter = max_iter;
   h.status = kRunning;
-  SK_CUDA_TRY(cudaMemcpyAsync(s.st, &h, sizeof(CgState), cudaMemcpyHostToDevice, stream));
-
-  // graph of `check_every` iterations
-  cudaGraphExec_t exec = nullptr;
-  {
-    cudaStream_t cap = stream ? stream : capture_stream();
-    cudaStream_t keep = s.stream;
-    s.stream = cap;
-    SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    int st = SK_OK;
-    for (int k = 0; k < check_every && st == SK_OK; ++k) {
-      st = s.launch_k1();
-      if (st == SK_OK) {
-        k2_update_rr<<<s.grid, kT, 0, cap>>>(n, s.p, s.q, x, s.r, s.st, s.partials);
-        k3_xpby<<<s.grid, kT, 0, cap>>>(n, s.r, s.p, s.st);
-      }
-    }
-    cudaGraph_t graph = nullptr;
-    cudaError_t e = cudaStreamEndCapture(cap, &graph);
-    s.stream = keep;
-    if (st != SK_OK) {
-      if (graph) cudaGraphDestroy(graph);
-      return st;
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-  }
-  struct GraphFree {
-    cudaGraphExec_t e;
-    ~GraphFree() {
-      if (e) cudaGraphExecDestroy(e);
-    }
-  } gfree{exec};
-  g_launches -= 3 * check_every;  // capture does not execute
+  SK_CUDA_TRY(cudaMemcpyAsync(s->st, &h, sizeof(CgState), cudaMemcpyHostToDevice, stream));
+  if (int e = s->ensure_graph(x, stream)) return e;
 
   int64_t restarts = 0;
   double rho = rho0;
@@ -326,16 +454,18 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
       if (opts.accept_recurrence) break;  // extension: report the true residual instead
       // recurrence says converged; accept only if the true residual agrees (:31-47)
       double true_res = 0;
-      if (int e = s.true_residual(x, b, &true_res)) return e;
+      if (int e = s->true_residual(x, b, &true_res, stream)) return e;
       if (true_res <= target) break;
-      k_restart<<<s.grid, kT, 0, stream>>>(n, b, s.q, s.r, s.p, s.st, s.partials);
+      k_restart<<<s->grid, kT, 0, stream>>>(n, b, s->q, s->r, s->p, s->st, s->partials);
       SK_LAUNCH_CHECK("k_restart");
       restarts++;
     }
-    SK_CUDA_TRY(cudaGraphLaunch(exec, stream));
-    g_launches += 3 * check_every;
-    SK_CUDA_TRY(cudaMemcpyAsync(&h, s.st, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
+    SK_CUDA_TRY(cudaGraphLaunch(s->exec, stream));
+    SK_CUDA_TRY(cudaMemcpyAsync(&h, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
+    // launched kernels: the loop runs one round past the last counted iteration
+    g_launches += int64_t(s->kernels_per_iteration()) *
+                  (s->device_loop ? (h.it - it + 1) : int64_t(s->check_every));
     it = h.it;
     rho = h.rho;
     status = h.status;
@@ -348,12 +478,12 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
     if (status == kMaxIter) break;
     if (status == kCheck) {
       h.status = kRunning;  // the check itself runs at the loop top
-      SK_CUDA_TRY(cudaMemcpyAsync(&s.st->status, &h.status, sizeof(int), cudaMemcpyHostToDevice, stream));
+      SK_CUDA_TRY(cudaMemcpyAsync(&s->st->status, &h.status, sizeof(int), cudaMemcpyHostToDevice, stream));
     }
   }
   // final acceptance on the true residual (:59-66)
   double res = 0;
-  if (int e = s.true_residual(x, b, &res)) return e;
+  if (int e = s->true_residual(x, b, &res, stream)) return e;
   report.iterations = it;
   report.restarts = restarts;
   report.true_rel_residual = res / bnorm;
@@ -365,13 +495,29 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
                                            std::to_string(res / bnorm));
   if (opts.deflate_mean) {  // :67-70
     double sum = 0;
-    if (int e = s.reduce<1>(x, &sum)) return e;
+    if (int e = s->reduce<1>(x, &sum, stream)) return e;
     const double mean = sum / double(n);
-    k_shift<<<s.grid, kT, 0, stream>>>(n, x, mean);
+    k_shift<<<s->grid, kT, 0, stream>>>(n, x, mean);
     SK_LAUNCH_CHECK("k_shift");
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
   }
   return SK_OK;
+}
+
+int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
+             cudaStream_t stream) {
+  if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
+  if (rep) *rep = sk_solve_report{0, 0, 0.0, 0.0};
+  if (m->rows == 0) return SK_OK;
+  CgOperator op;
+  op.m = m;
+  op.n = m->rows;
+  CgPlan* plan = nullptr;
+  if (int e = cg_plan_create(op, o ? o->check_every : 0, stream, &plan)) return e;
+  const int st = cg_plan_solve(plan, b, x, o, rep, stream);
+  cudaStreamSynchronize(stream);  // the workspace is freed synchronously
+  cg_plan_destroy(plan);
+  return st;
 }
 
 }  // namespace sk

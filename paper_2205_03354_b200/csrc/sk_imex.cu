@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -34,6 +35,11 @@ struct sk_ch_imex {
   sk_csr* L = nullptr;
   sk_csr* B = nullptr;
   sk_csr* A = nullptr;  // identity_plus_scaled(B, a_factor)
+  // matrix-free CG operator: the stencil of A (same weights as A's CSR
+  // values, applied by the streaming stencil kernels: no matrix traffic)
+  bool matrix_free = false;
+  sk_stencil* a_st = nullptr;
+  sk::CgPlan* plan = nullptr;
   double a_factor = 0.0;
   int a_order = 0;
   double* chem = nullptr;  // L f'(c) of this step
@@ -43,6 +49,8 @@ struct sk_ch_imex {
   bool have_prev = false;
   double prev_dt = 0.0;
   ~sk_ch_imex() {
+    sk::cg_plan_destroy(plan);
+    sk_stencil_destroy(a_st);
     sk_csr_destroy(A);
     sk_csr_destroy(B);
     sk_csr_destroy(L);
@@ -153,7 +161,7 @@ __global__ void k_ips_fill(int64_t rows, const int64_t* __restrict__ rp, const I
 int grid_for(int64_t n) { return int(std::min<int64_t>((n + kT - 1) / kT, int64_t(num_sms()) * 8)); }
 
 template <class Idx>
-int ips_build(const sk_csr* b, double alpha, sk_csr** out, cudaStream_t s) {
+int ips_build(const sk_csr* b, double alpha, sk_csr** out, cudaStream_t s, bool sell) {
   const int64_t rows = b->rows;
   const Idx* col = static_cast<const Idx*>(b->col);
   int64_t* cnt = nullptr;
@@ -193,7 +201,7 @@ int ips_build(const sk_csr* b, double alpha, sk_csr** out, cudaStream_t s) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) st = cuda_fail(e, "k_ips_fill");
   }
-  if (st == SK_OK) st = csr_build_sell(m, s);
+  if (st == SK_OK && sell) st = csr_build_sell(m, s);
   if (st != SK_OK) {
     delete m;
     return st;
@@ -202,9 +210,10 @@ int ips_build(const sk_csr* b, double alpha, sk_csr** out, cudaStream_t s) {
   return SK_OK;
 }
 
-int identity_plus_scaled(const sk_csr* b, double alpha, sk_csr** out, cudaStream_t s) {
+// sell: also build the SELL copy the CSR CG operator reads
+int identity_plus_scaled(const sk_csr* b, double alpha, sk_csr** out, cudaStream_t s, bool sell) {
   if (b->rows != b->cols) return fail(SK_ERR_SHAPE_MISMATCH, "needs a square matrix");
-  return b->index_bits == 32 ? ips_build<int32_t>(b, alpha, out, s) : ips_build<int64_t>(b, alpha, out, s);
+  return b->index_bits == 32 ? ips_build<int32_t>(b, alpha, out, s, sell) : ips_build<int64_t>(b, alpha, out, s, sell);
 }
 
 // laplacian(dim, 2) (generators.cpp:94-108) and compose(L, L) (stencil.cpp:75-87):
@@ -300,6 +309,15 @@ int sk_ch_imex_create(const sk_grid_desc* gd, const sk_ch_params* p, const sk_so
     if (st == SK_OK && cudaMalloc(reinterpret_cast<void**>(q), bytes) != cudaSuccess)
       st = fail(SK_ERR_OUT_OF_MEMORY, "IMEX work vectors");
   if (st == SK_OK) st = csr_build_sell(s->B, hs);
+  // matrix-free implicit operator on the kernels' symmetric radius-2 classes
+  // (grid at least the stencil width: no wrapped duplicates) unless
+  // SK_IMEX_MATRIX_FREE=0 (CSR SpMV, bit-identical products)
+  if (st == SK_OK) {
+    const char* env = getenv("SK_IMEX_MATRIX_FREE");
+    bool wide = true;
+    for (int a = 0; a < g.dim; ++a) wide &= g.n[a] >= 5;
+    s->matrix_free = wide && (s->bilap->kclass == 1 || s->bilap->kclass == 2) && !(env && env[0] == '0');
+  }
   if (st == SK_OK && cudaStreamSynchronize(hs) != cudaSuccess) st = fail(SK_ERR_CUDA, "IMEX setup");
   if (st != SK_OK) {
     delete s;
@@ -347,9 +365,39 @@ int sk_ch_imex_step(sk_ch_imex* s, double* c, double dt, int order, int64_t nste
     // ensure_implicit_matrix (:131-137)
     const double factor = dt * M * kappa * (eff == 2 ? 0.5 : 1.0);
     if (!s->A || s->a_factor != factor || s->a_order != eff) {
+      cg_plan_destroy(s->plan);
+      s->plan = nullptr;
       sk_csr_destroy(s->A);
       s->A = nullptr;
-      if (int e = identity_plus_scaled(s->B, factor, &s->A, st)) return e;
+      sk_stencil_destroy(s->a_st);
+      s->a_st = nullptr;
+      if (int e = identity_plus_scaled(s->B, factor, &s->A, st, !s->matrix_free)) return e;
+      CgOperator op;
+      op.n = n;
+      if (s->matrix_free) {
+        // A's weights exactly as identity_plus_scaled forms its values:
+        // alpha * (coeff * pow_int(h, h_power)) (+ 1.0 on the centre), h_power 0
+        const sk_stencil* b = s->bilap;
+        const double scale = pow_int(s->g.h, b->h_power);
+        std::vector<int32_t> off(size_t(b->nent) * size_t(s->g.dim));
+        std::vector<double> co(size_t(b->nent));
+        for (int e = 0; e < b->nent; ++e) {
+          bool centre = true;
+          for (int a = 0; a < s->g.dim; ++a) {
+            off[size_t(e) * size_t(s->g.dim) + size_t(a)] = b->off[size_t(e) * 3 + size_t(a)];
+            centre &= b->off[size_t(e) * 3 + size_t(a)] == 0;
+          }
+          double v = factor * (b->coeff[size_t(e)] * scale);
+          if (centre) v += 1.0;
+          co[size_t(e)] = v;
+        }
+        if (int e = sk_stencil_create(s->g.dim, b->nent, off.data(), co.data(), 0, &s->a_st)) return e;
+        op.s = s->a_st;
+        op.g = s->g;
+      } else {
+        op.m = s->A;
+      }
+      if (int e = cg_plan_create(op, s->opts.check_every, st, &s->plan)) return e;
       s->a_factor = factor;
       s->a_order = eff;
     }
@@ -366,7 +414,7 @@ int sk_ch_imex_step(sk_ch_imex* s, double* c, double dt, int order, int64_t nste
     sk_solve_report rep{};
     sk_solve_options o = s->opts;
     o.use_initial_guess = 0;  // cg_solve starts from x0 = 0 (linalg.cpp:22)
-    if (int e = sk_cg_solve(s->A, s->rhs, c, &o, &rep, st)) return e;
+    if (int e = cg_plan_solve(s->plan, s->rhs, c, &o, &rep, st)) return e;
     if (last) *last = rep;
     if (cg_iterations) *cg_iterations += rep.iterations;
     if (order == 2) {  // (:183-188)

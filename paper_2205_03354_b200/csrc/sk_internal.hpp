@@ -61,6 +61,24 @@ int check_width(const sk_stencil* s, const GridInfo& g);
 // Launch one matrix-free application on `stream` (device pointers).
 int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream);
 
+// ---- conjugate gradients (sk_cg.cu) ----
+// The operator q = A p: an assembled CSR (SELL SpMV, bit-identical to the
+// reference's csr_matvec) or a matrix-free stencil on a periodic grid.
+struct CgOperator {
+  const sk_csr* m = nullptr;
+  const sk_stencil* s = nullptr;
+  GridInfo g{};
+  int64_t n = 0;
+};
+// Workspace + captured iteration graph, reusable across solves.
+struct CgPlan;
+int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, CgPlan** out);
+void cg_plan_destroy(CgPlan* p);
+int cg_plan_solve(CgPlan* p, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
+                  cudaStream_t stream);
+int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
+             cudaStream_t stream);
+
 // Internal per-thread non-blocking stream: graph capture when the caller
 // passes the legacy stream, and the stream every *_host entry point runs on.
 cudaStream_t capture_stream();

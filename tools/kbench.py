@@ -93,6 +93,24 @@ def main():
             y = DeviceArray(m.rows)
             ms = timer(lib, lambda: csr_matvec(m, x, y), args.reps)
             byts = (8 + bits // 8) * m.nnz() + 8.0 * (m.rows + 1) + 16.0 * m.rows
+    elif case.startswith("imex"):  # imex2d / imex3d: IMEX CH steps (reference's own CH path), order 2
+        from paper_2205_03354_b200.cahn_hilliard import CahnHilliardParams, CahnHilliardStepper, ch_init
+
+        dim = 3 if case == "imex3d" else 2
+        n = args.n or (1024 if dim == 2 else 128)
+        g = make_periodic_grid(dim, n, 1.0)
+        st = CahnHilliardStepper(g, CahnHilliardParams())
+        c = DeviceArray.from_host(ch_init(g).c)
+        st.step_device(c, 0.05, 2, 2)  # bootstrap + build both implicit matrices
+        its = []
+
+        def one():
+            st.step_device(c, 0.05, 2, 1)
+            its.append(st.last_cg_iterations)
+
+        ms = timer(lib, one, args.reps)
+        print(f"{case}: n={n}^{dim} CG iterations/step {np.mean(its):.1f}")
+        byts = 16.0 * g.unknown_count()
     else:
         raise SystemExit(f"unknown case {case}")
     print(f"{case}: {ms * 1e3:.2f} us/launch, {byts / (ms * 1e-3) / 1e9:.1f} GB/s algorithmic")
