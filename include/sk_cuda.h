@@ -208,6 +208,19 @@ int sk_ch_imex_matrix(const sk_ch_imex* s, int which, const sk_csr** out);
 /* ch_init (cahn_hilliard.cpp:20-63) on the host, bit-identical (origin 0). */
 int sk_ch_init_host(const sk_grid_desc* g, double c0, double eps_ic, double* c_host);
 
+/* ---- spectral tools (linalg.cpp:74-106, 149-222) -------------------------
+ * power_iteration: |Rayleigh quotient| of M from a seeded mt19937_64 start,
+ * geometric-tail stopping rule; SK_ERR_NO_CONVERGENCE past max_iter.
+ * periodic_spectrum: eigenvalues (affine_shift + affine_scale * h^s * symbol)
+ * of every Fourier mode on an all-periodic grid (eigen_host: 2 doubles per
+ * mode, x-fastest mode order, may be NULL), the spectral radius, the
+ * continuous-torus symbol radius and max|ev| / min nonzero |ev|. */
+int sk_power_iteration(const sk_csr* m, double tol, uint64_t seed, int64_t max_iter, double* out,
+                       int64_t* iterations, void* stream);
+int sk_periodic_spectrum(const sk_stencil* s, const sk_grid_desc* g, double affine_shift, double affine_scale,
+                         double* eigen_host, double* spectral_radius, double* symbol_radius,
+                         double* condition_estimate);
+
 /* ---- CSR assembly (grid.cpp:62-158) and SpMV (kernels.cpp:8-17) --------- */
 int sk_csr_assemble(const sk_stencil* s, const sk_grid_desc* g, int index_bits, sk_csr** out,
                     void* stream);

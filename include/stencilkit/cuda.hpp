@@ -319,6 +319,30 @@ inline void imex_step(CahnHilliardStepper& stepper, CahnHilliardState& s, double
   stepper.step(s, dt, order);
 }
 
+/// power_iteration (linalg.cpp:74-106): the loop runs on the device.
+inline double power_iteration(const DeviceCsr& m, double tol, std::uint64_t seed = 20240801,
+                              std::int64_t max_iter = 2'000'000) {
+  double out = 0;
+  check(sk_power_iteration(m.get(), tol, seed, max_iter, &out, nullptr, nullptr));
+  return out;
+}
+inline double power_iteration(const CsrMatrix& m, double tol, std::uint64_t seed = 20240801,
+                              std::int64_t max_iter = 2'000'000) {
+  return power_iteration(DeviceCsr(m), tol, seed, max_iter);
+}
+
+/// periodic_spectrum (linalg.cpp:149-222): modes and sampling on the device.
+inline SpectrumReport periodic_spectrum(const Stencil& s, const GridSpec& g, double affine_shift = 0.0,
+                                        double affine_scale = 1.0) {
+  const DeviceStencil ds(s);
+  const sk_grid_desc d = grid_desc(g);
+  SpectrumReport rep;
+  rep.eigenvalues.resize(static_cast<size_t>(g.unknown_count()));
+  check(sk_periodic_spectrum(ds.get(), &d, affine_shift, affine_scale, reinterpret_cast<double*>(rep.eigenvalues.data()),
+                             &rep.spectral_radius, &rep.symbol_radius, &rep.condition_estimate));
+  return rep;
+}
+
 /// ch_init (cahn_hilliard.cpp:20-63), bit-identical (origin 0 grids).
 inline CahnHilliardState ch_init(const GridSpec& grid, const CahnHilliardParams& p) {
   CahnHilliardState s;

@@ -79,6 +79,9 @@ class Oracle:
         L.sko_ch_init.argtypes = [C.c_int, i64, dbl, dbl, dbl, vp]
         L.sko_ch_imex_seq.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int, vp, vp, vp, vp]
         L.sko_identity_plus_scaled.argtypes = [C.POINTER(SkoCsr), dbl, C.POINTER(SkoCsr)]
+        L.sko_power_iteration.argtypes = [C.POINTER(SkoCsr), dbl, C.c_uint64, i64, C.POINTER(dbl), C.POINTER(i64)]
+        L.sko_periodic_eigen.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, dbl, dbl, dbl, vp, C.POINTER(dbl),
+                                         C.POINTER(dbl)]
         L.sko_free_energy.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, vp]
         L.sko_free_energy.restype = dbl
         L.sko_biharmonic_clamped.argtypes = [C.c_int, i64, vp, vp]
@@ -187,6 +190,31 @@ class Oracle:
         out = np.empty(n ** dim)
         self.L.sko_ch_init(dim, n, h, c0, eps, _p(out))
         return out
+
+    def power_iteration(self, rp, ci, vals, tol, seed=20240801, max_iter=2_000_000):
+        m = SkoCsr()
+        rp = np.ascontiguousarray(rp, np.int64)
+        ci = np.ascontiguousarray(ci, np.int64)
+        vals = np.ascontiguousarray(vals, np.float64)
+        m.rows = m.cols = rp.size - 1
+        m.nnz = ci.size
+        m.row_ptr = rp.ctypes.data_as(C.POINTER(C.c_int64))
+        m.col_idx = ci.ctypes.data_as(C.POINTER(C.c_int64))
+        m.values = vals.ctypes.data_as(C.POINTER(C.c_double))
+        out, its = dbl(), i64()
+        if self.L.sko_power_iteration(C.byref(m), tol, seed, max_iter, C.byref(out), C.byref(its)):
+            raise ValueError("oracle power iteration did not settle")
+        return out.value, its.value
+
+    def periodic_eigen(self, stencil, grid, shift=0.0, scale=1.0):
+        off, co = _flat(stencil)
+        n, _ = _grid_arrays(grid)
+        modes = int(np.prod(n[: stencil.dim]))
+        eig = np.empty(2 * modes)
+        rho, cond = dbl(), dbl()
+        self.L.sko_periodic_eigen(stencil.dim, co.size, _p(off), _p(co), stencil.h_power, _p(n), grid.h, shift, scale,
+                                  _p(eig), C.byref(rho), C.byref(cond))
+        return eig.view(np.complex128), rho.value, cond.value
 
     def identity_plus_scaled(self, rp, ci, vals, alpha):
         m, out = SkoCsr(), SkoCsr()
@@ -309,6 +337,9 @@ class Reference:
         L.skref_imex_steps.argtypes = [vp, dbl, C.c_int, C.c_longlong, vp]
         L.skref_imex_free.argtypes = [vp]
         L.skref_ch_init.argtypes = [C.c_int, C.c_int, dbl, dbl, dbl, vp]
+        L.skref_power_iteration.argtypes = [vp, dbl, C.c_ulonglong, C.c_longlong, C.POINTER(dbl)]
+        L.skref_periodic_spectrum.argtypes = [C.c_int, C.c_int, C.c_int, vp, dbl, dbl, dbl, vp, C.POINTER(dbl),
+                                              C.POINTER(dbl), C.POINTER(dbl)]
         L.skref_identity_plus_scaled.argtypes = [vp, dbl]
         L.skref_identity_plus_scaled.restype = vp
         self.L = L
@@ -399,6 +430,15 @@ class Reference:
 
     def imex_free(self, handle) -> None:
         self.L.skref_imex_free(handle)
+
+    def periodic_spectrum(self, dim, acc, kind, n, h, shift=0.0, scale=1.0):
+        na = np.ascontiguousarray(list(n) + [1] * (3 - len(n)), np.int32)
+        eig = np.empty(2 * int(np.prod(n)))
+        rho, sym, cond = dbl(), dbl(), dbl()
+        if self.L.skref_periodic_spectrum(dim, acc, kind, _p(na), h, shift, scale, _p(eig), C.byref(rho),
+                                          C.byref(sym), C.byref(cond)):
+            raise RuntimeError(self.err())
+        return eig.view(np.complex128), rho.value, sym.value, cond.value
 
     def ch_init(self, dim, n, h, c0, eps) -> np.ndarray:
         out = np.empty(n ** dim)

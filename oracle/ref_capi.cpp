@@ -435,6 +435,36 @@ void* skref_identity_plus_scaled(void* mp, double alpha) {
   return new CsrMatrix(identity_plus_scaled(*static_cast<CsrMatrix*>(mp), alpha));
 }
 
+// power_iteration (linalg.cpp:74-106) on an assembled handle
+int skref_power_iteration(void* mp, double tol, unsigned long long seed, long long max_iter, double* out) {
+  try {
+    *out = power_iteration(*static_cast<CsrMatrix*>(mp), tol, seed, max_iter);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+// periodic_spectrum (linalg.cpp:149-222) of build_stencil(dim, acc, kind)
+int skref_periodic_spectrum(int dim, int acc, int kind, const int* n, double h, double shift, double scale,
+                            double* eig, double* rho, double* sym, double* cond) {
+  try {
+    GridSpec g = make_periodic_grid(dim, n[0], h);
+    for (int a = 0; a < dim; ++a) g.n[static_cast<size_t>(a)] = n[a];
+    SpectrumReport r = periodic_spectrum(build_stencil(dim, acc, kind), g, shift, scale);
+    for (size_t i = 0; i < r.eigenvalues.size(); ++i) {
+      eig[2 * i] = r.eigenvalues[i].real();
+      eig[2 * i + 1] = r.eigenvalues[i].imag();
+    }
+    *rho = r.spectral_radius;
+    *sym = r.symbol_radius;
+    *cond = r.condition_estimate;
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
 double skref_free_energy(int dim, int n, double h, double kappa, double rho_w, double c_alpha,
                          double c_beta, const double* c, int serial) {
   CahnHilliardState st;

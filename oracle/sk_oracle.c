@@ -559,6 +559,89 @@ int sko_ch_imex(int dim, int64_t n, double h, double mobility, double kappa, dou
   return sko_ch_imex_seq(dim, n, h, mobility, kappa, rho_w, c_alpha, c_beta, rel_tol, 1, &dt, &order, &nsteps, c);
 }
 
+/* power_iteration (linalg.cpp:74-106), serial reductions */
+int sko_power_iteration(const sko_csr* m, double tol, uint64_t seed, int64_t max_iter, double* out,
+                        int64_t* iterations) {
+  const int64_t n = m->rows;
+  double* v = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double* w = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  sko_uniform(seed, n, -1.0, 1.0, v);
+  const double nv = sko_nrm2(n, v);
+  for (int64_t i = 0; i < n; ++i) v[i] /= nv;
+  double lambda = 0, prev = 0, prev_delta = 0;
+  int st = 1;
+  *out = 0;
+  for (int64_t it = 0; it < max_iter; ++it) {
+    if (iterations) *iterations = it + 1;
+    sko_csr_matvec(m, v, w);
+    lambda = sko_dot(n, v, w);
+    const double wn = sko_nrm2(n, w);
+    if (wn == 0.0) {
+      st = 0;
+      break;
+    }
+    for (int64_t i = 0; i < n; ++i) v[i] = w[i] / wn;
+    if (it > 0) {
+      const double delta = fabs(lambda - prev);
+      if (it > 1 && prev_delta > 0 && delta < prev_delta) {
+        const double r = delta / prev_delta;
+        const double tail = delta * r / (1.0 - r);
+        if (tail <= 0.25 * tol * fabs(lambda)) {
+          *out = fabs(lambda);
+          st = 0;
+          break;
+        }
+      }
+      if (delta == 0.0) {
+        *out = fabs(lambda);
+        st = 0;
+        break;
+      }
+    }
+    prev_delta = it > 0 ? fabs(lambda - prev) : 0;
+    prev = lambda;
+  }
+  free(v);
+  free(w);
+  return st;
+}
+
+/* periodic_spectrum eigenvalues (linalg.cpp:160-181) and the radius /
+ * condition reductions (:183-193); eig: 2 doubles per mode */
+void sko_periodic_eigen(int dim, int nent, const int* off, const double* coeff, int h_power, const int64_t* n,
+                        double h, double shift, double scale, double* eig, double* rho_out, double* cond_out) {
+  const double two_pi = 2 * 3.141592653589793;
+  const double scale_total = scale * pow_int(h, h_power);
+  int64_t modes = 1;
+  for (int a = 0; a < dim; ++a) modes *= n[a];
+  double rho = 0, min_nz = 0;
+  for (int64_t m = 0; m < modes; ++m) {
+    int64_t rem = m;
+    double theta[3];
+    for (int a = 0; a < dim; ++a) {
+      theta[a] = two_pi * (double)(rem % n[a]) / (double)n[a];
+      rem /= n[a];
+    }
+    double re = 0, im = 0;
+    for (int e = 0; e < nent; ++e) {
+      double phase = 0;
+      for (int a = 0; a < dim; ++a) phase += theta[a] * off[e * dim + a];
+      re += coeff[e] * cos(phase);
+      im += coeff[e] * sin(phase);
+    }
+    eig[2 * m] = shift + scale_total * re;
+    eig[2 * m + 1] = scale_total * im;
+    const double mag = hypot(eig[2 * m], eig[2 * m + 1]);
+    if (mag > rho) rho = mag;
+  }
+  for (int64_t m = 0; m < modes; ++m) {
+    const double mag = hypot(eig[2 * m], eig[2 * m + 1]);
+    if (mag > 1e-12 * rho && (min_nz == 0 || mag < min_nz)) min_nz = mag;
+  }
+  *rho_out = rho;
+  *cond_out = min_nz > 0 ? rho / min_nz : 0;
+}
+
 /* ch_init (cahn_hilliard.cpp:20-63), origin 0 */
 void sko_ch_init(int dim, int64_t n, double h, double c0, double eps, double* out) {
   if (dim == 2) {

@@ -72,3 +72,39 @@ def cg_solve(m: CsrMatrix, b, opts: SolveOptions | None = None, report: SolveRep
             report.restarts = rep.restarts
             report.true_rel_residual = rep.true_rel_residual
             report.recurrence_rel_residual = rep.recurrence_rel_residual
+
+
+# ------------------------------------------------------------ spectral --
+def power_iteration(m: CsrMatrix, tol: float, seed: int = 20240801, max_iter: int = 2_000_000,
+                    stream=None) -> float:
+    """power_iteration (linalg.cpp:74-106): |Rayleigh quotient| from a seeded
+    mt19937_64 start, geometric-tail stopping rule, the loop on the device."""
+    if m.rows != m.cols:
+        raise StencilkitError(Errc.shape_mismatch, "power iteration needs a square matrix")
+    out, its = C.c_double(), C.c_int64()
+    check(m.lib.sk_power_iteration(m.handle, tol, seed, max_iter, C.byref(out), C.byref(its), stream))
+    power_iteration.last_iterations = its.value
+    return out.value
+
+
+@dataclass
+class SpectrumReport:
+    """linalg.hpp SpectrumReport"""
+    eigenvalues: np.ndarray = None  # complex128, one per Fourier mode (x fastest)
+    spectral_radius: float = 0.0
+    symbol_radius: float = 0.0
+    condition_estimate: float = 0.0  # max|lambda| / min nonzero |lambda|
+
+
+def periodic_spectrum(stencil, grid, affine_shift: float = 0.0, affine_scale: float = 1.0) -> SpectrumReport:
+    """periodic_spectrum (linalg.cpp:149-222) on the device."""
+    from .grid import DeviceStencil
+
+    ds = stencil if isinstance(stencil, DeviceStencil) else DeviceStencil(stencil)
+    grid.validate()
+    d = grid.desc()
+    ev = np.empty(2 * grid.unknown_count())
+    rho, sym, cond = C.c_double(), C.c_double(), C.c_double()
+    check(ds.lib.sk_periodic_spectrum(ds.handle, C.byref(d), affine_shift, affine_scale, ev.ctypes.data,
+                                      C.byref(rho), C.byref(sym), C.byref(cond)))
+    return SpectrumReport(ev.view(np.complex128), rho.value, sym.value, cond.value)

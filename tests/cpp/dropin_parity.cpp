@@ -177,6 +177,18 @@ int main() {
     }
     EXPECT(std::sqrt(d) <= 1e-9 * std::sqrt(nn) && g.t == r.t, "IMEX stepper (orders 1/2, AB2 history) within 1e-9");
   }
+  {  // spectral tools: the reference's own known answers (test_linalg.cpp:74-145)
+    const Stencil bil = compose(laplacian(2, 2), laplacian(2, 2));  // builtin "bilaplacian-2d"
+    const GridSpec g20 = make_periodic_grid(2, 20, 10.0);
+    const double rho = cuda::power_iteration(assemble(bil, g20), 1e-8);
+    const SpectrumReport r = periodic_spectrum(bil, g20), c = cuda::periodic_spectrum(bil, g20);
+    EXPECT(std::abs(rho - r.spectral_radius) <= 1e-6 * r.spectral_radius, "power_iteration within 1e-6");
+    EXPECT(c.spectral_radius == r.spectral_radius && c.symbol_radius == r.symbol_radius,
+           "periodic_spectrum radii identical to the reference");
+    const SpectrumReport t = cuda::periodic_spectrum(bil, make_periodic_grid(2, 50, 4.0), 1.0, 1.0);
+    EXPECT(t.symbol_radius == 1.25 && t.spectral_radius == 1.25 && t.condition_estimate == 1.25,
+           "time-stepping table row h=4 exact");
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

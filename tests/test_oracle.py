@@ -277,3 +277,28 @@ def test_oracle_identity_plus_scaled_vs_reference(orc, ref):
     assert r.tolist() == [0, 3, 5, 7]
     assert c.tolist() == [0, 1, 2, 0, 1, 1, 2]
     assert vals.tolist() == [1.0, 0.5, 1.0, 1.5, 1.0, 2.0, 1.0]
+
+
+# --------------------------------------------------------- spectral (§8f 2) --
+def test_oracle_spectral_vs_reference(orc, ref):
+    # periodic_spectrum eigenvalues / radius / condition and power_iteration
+    # (linalg.cpp:74-106,149-193): the C restatement equals the reference
+    import ctypes
+
+    from oracle.ffi import RefCsr
+    from paper_2205_03354_b200.stencil import bilaplacian, laplacian
+
+    ref.L.skref_set_threads(1)
+    for dim, acc, kind, n, h in [(2, 2, 2, (12, 10), 0.5), (3, 2, 2, (6, 5, 7), 1.0), (1, 2, 1, (16,), 0.25),
+                                 (2, 4, 2, (9, 9), 1.0)]:
+        s = bilaplacian(dim, acc) if kind == 2 else laplacian(dim, acc)
+        g = GridSpec(dim=dim, n=list(n), h=h, origin=[0.0] * dim, bc=[BoundaryKind.periodic] * dim)
+        for shift, scale in [(0.0, 1.0), (1.0, 0.25)]:
+            e_ref, rho_ref, _sym, cond_ref = ref.periodic_spectrum(dim, acc, kind, n, h, shift, scale)
+            e, rho, cond = orc.periodic_eigen(s, g, shift, scale)
+            assert np.array_equal(e, e_ref) and rho == rho_ref and cond == cond_ref
+        m = RefCsr(ref, dim, acc, kind, list(n), h, [0] * dim)
+        out = ctypes.c_double()
+        assert ref.L.skref_power_iteration(m.h, 1e-8, 20240801, 2_000_000, ctypes.byref(out)) == 0
+        lam, its = orc.power_iteration(*m.arrays(), 1e-8)
+        assert lam == out.value, (lam, out.value)
