@@ -239,6 +239,22 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         const double2 r0 = ld2(cn), r1 = ld2(cn + P);
         Cz[C0][0] = r0.x; Cz[C0][1] = r0.y; Cz[C0][2] = r1.x; Cz[C0][3] = r1.y;
       }
+      // neighbour values of the output's mu plane (k-2), issued first: they
+      // only depend on the previous step's mu slot and the own mu registers
+      double olf0 = 0, olf1 = 0, ort0 = 0, ort1 = 0;
+      double2 oup = make_double2(0, 0), odn = make_double2(0, 0);
+      if constexpr (DO_OUT && V == 0) {
+        const double* m2 = M[M2];
+        const double* mb = mu_ring + M2 * SM::MU_PLANE + mofs;  // slot of plane k-2
+        olf0 = __shfl_up_sync(0xffffffffu, m2[1], 1);
+        olf1 = __shfl_up_sync(0xffffffffu, m2[3], 1);
+        ort0 = __shfl_down_sync(0xffffffffu, m2[0], 1);
+        ort1 = __shfl_down_sync(0xffffffffu, m2[2], 1);
+        if (lane == 0) { olf0 = mb[-1]; olf1 = mb[MP - 1]; }
+        if (lane == 31) { ort0 = mb[2]; ort1 = mb[MP + 2]; }
+        oup = ld2(mb - MP);
+        odn = ld2(mb + 2 * MP);
+      }
       if constexpr (DO_MU && V == 1) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) M[M1][i] = Cz[C1][i];
@@ -265,13 +281,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         double* mb = mu_ring + M1 * SM::MU_PLANE + mofs;  // slot of plane k-1
         *reinterpret_cast<double2*>(mb) = make_double2(m1[0], m1[1]);
         *reinterpret_cast<double2*>(mb + MP) = make_double2(m1[2], m1[3]);
-        if (has_ex) {  // one border point of the mu tile
-          const double* rb = ring + s_k1 * PLANE + ex_c;
-          const double cc = rb[0];
-          const double sr = ((ring[s_k2 * PLANE + ex_c] + ring[s_k * PLANE + ex_c]) + (rb[-1] + rb[1])) +
-                            (rb[-P] + rb[P]);
-          mu_ring[M1 * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
-        }
       }
       if constexpr (DO_OUT) {  // output plane k-2
         const double* c2 = Cz[C2];
@@ -283,16 +292,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           const double* m1 = M[M1];
           const double* m2 = M[M2];
           const double* m3 = M[M3];
-          const double* mb = mu_ring + M2 * SM::MU_PLANE + mofs;  // slot of plane k-2
-          double lf0 = __shfl_up_sync(0xffffffffu, m2[1], 1), lf1 = __shfl_up_sync(0xffffffffu, m2[3], 1);
-          double rt0 = __shfl_down_sync(0xffffffffu, m2[0], 1), rt1 = __shfl_down_sync(0xffffffffu, m2[2], 1);
-          if (lane == 0) { lf0 = mb[-1]; lf1 = mb[MP - 1]; }
-          if (lane == 31) { rt0 = mb[2]; rt1 = mb[MP + 2]; }
-          const double2 up = ld2(mb - MP), dn = ld2(mb + 2 * MP);
-          const double s00 = ((m3[0] + m1[0]) + (lf0 + m2[1])) + (up.x + m2[2]);
-          const double s01 = ((m3[1] + m1[1]) + (m2[0] + rt0)) + (up.y + m2[3]);
-          const double s10 = ((m3[2] + m1[2]) + (lf1 + m2[3])) + (m2[0] + dn.x);
-          const double s11 = ((m3[3] + m1[3]) + (m2[2] + rt1)) + (m2[1] + dn.y);
+          const double s00 = ((m3[0] + m1[0]) + (olf0 + m2[1])) + (oup.x + m2[2]);
+          const double s01 = ((m3[1] + m1[1]) + (m2[0] + ort0)) + (oup.y + m2[3]);
+          const double s10 = ((m3[2] + m1[2]) + (olf1 + m2[3])) + (m2[0] + odn.x);
+          const double s11 = ((m3[3] + m1[3]) + (m2[2] + ort1)) + (m2[1] + odn.y);
           o[0] = fma(a.wl1, s00, fma(a.wl0, m2[0], c2[0]));
           o[1] = fma(a.wl1, s01, fma(a.wl0, m2[1], c2[1]));
           o[2] = fma(a.wl1, s10, fma(a.wl0, m2[2], c2[2]));
@@ -324,6 +327,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           }
         }
         outp += opp;
+      }
+      if constexpr (DO_MU && V == 0) {
+        if (has_ex) {  // one border point of the mu tile (needed from the next step on)
+          const double* rb = ring + s_k1 * PLANE + ex_c;
+          const double cc = rb[0];
+          const double sr = ((ring[s_k2 * PLANE + ex_c] + ring[s_k * PLANE + ex_c]) + (rb[-1] + rb[1])) +
+                            (rb[-P] + rb[P]);
+          mu_ring[M1 * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
+        }
       }
       if (++s_k == S) {
         s_k = 0;
