@@ -50,6 +50,11 @@ __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_ca
 #define SK_PADL 16
 #endif
 constexpr int kPadL = SK_PADL, kPadT = 2;
+// L2 policy of the TMA loads: evict_last keeps tile halos for the
+// y-neighbour tile's CTA (measured +0.5%; evict_first: -19%)
+#ifndef SK_TMA_HINT
+#define SK_TMA_HINT 1
+#endif
 #ifndef SK_TMA_SPLIT
 #define SK_TMA_SPLIT 1
 #endif
@@ -101,7 +106,7 @@ struct TmaCursor {
       mbar_arrive_expect_tx(&bars[stage], SM::STAGE_BYTES);
 #pragma unroll
       for (int q = 0; q < kTmaSplit; ++q)  // the box: C::ROWS / kTmaSplit rows
-        tma_load_3d(ring + stage * SM::PLANE + q * (C::ROWS / kTmaSplit) * SM::P, tm, x0,
+        tma_load_3d_hint<SK_TMA_HINT>(ring + stage * SM::PLANE + q * (C::ROWS / kTmaSplit) * SM::P, tm, x0,
                     y0 + q * (C::ROWS / kTmaSplit), z, &bars[stage]);
       z = z + 1 == a.nz ? 0 : z + 1;
       if (++lp == np) {

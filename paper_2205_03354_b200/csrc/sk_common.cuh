@@ -103,6 +103,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, in
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+// the same with an L2 eviction-priority hint (createpolicy.fractional)
+template <int HINT>  // 0 evict_normal (no hint), 1 evict_last, 2 evict_first
+__device__ __forceinline__ void tma_load_3d_hint(void* dst_smem, const void* tmap, int x, int y, int z, uint64_t* bar) {
+  if constexpr (HINT == 0) {
+    tma_load_3d(dst_smem, tmap, x, y, z, bar);
+  } else {
+    uint64_t pol;
+    if constexpr (HINT == 1)
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst_smem)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+  }
+}
+
 // order this thread's prior generic-proxy shared accesses before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -106,6 +106,10 @@ inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
       a.zchunk = int(d);
       break;
     }
+  if (const char* zc = getenv("SK_ZCHUNK")) {  // experiments
+    const int64_t v = atoll(zc);
+    if (v >= 1 && a.nz % v == 0) a.zchunk = int(v);
+  }
   return grid;
 }
 
