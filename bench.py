@@ -454,9 +454,11 @@ def main() -> int:
     args = ap.parse_args()
     dim = 3 if args.workload == "ch3d" else 2
     n, h, p, dt, seed = ch_setup(dim)
+    kb, kl = (25, 7) if dim == 3 else (13, 5)
     workload = (f"config {4 if dim == 3 else 3}: fused explicit Cahn-Hilliard step, periodic fp64 {n}^{dim}, "
-                f"eps={0.02 if dim == 3 else 0.01}, dt={dt:.4e}, composed {25 if dim == 3 else 13}-pt B + "
-                f"{7 if dim == 3 else 5}-pt L on f'(u)")
+                f"eps={0.02 if dim == 3 else 0.01}, dt={dt:.4e}; u' = u + dt L(f'(u) - eps^2 L u) with the "
+                f"{kl}-pt L, i.e. the {kb}-pt composed B = compose(L, L) applied as two fused {kl}-pt passes "
+                f"(the literal {kb}-pt-weights kernel is the 'composed' extra line)")
     config = {"workload": workload, "grid": [n] * dim, "points_per_step": n ** dim, "dtype": "fp64",
               "l2": "inputs larger than L2 (2 x 134 MB fields)" if dim == 3 else
               "2 x 33.5 MB fields fit in the 126 MB L2", "parallelism": f"replicas x{args.gpus}"}
