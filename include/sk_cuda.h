@@ -229,6 +229,10 @@ int sk_csr_upload(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_pt
 int sk_csr_info(const sk_csr* m, int64_t* rows, int64_t* cols, int64_t* nnz, int* index_bits);
 int sk_csr_download(const sk_csr* m, int64_t* row_ptr, int64_t* col_idx, double* values);
 int sk_csr_destroy(sk_csr* m);
+/* out = b * a (csr_matmul, linalg.cpp:253-283): per-row products summed per
+ * column in the reference's order (bit-identical values), exact zeros
+ * dropped, columns sorted. Device limit: 1024 products per row. */
+int sk_csr_matmul(const sk_csr* b, const sk_csr* a, sk_csr** out, void* stream);
 /* y = M x, per-row sequential accumulation in column order (bit-identical to
  * the reference's serial csr_matvec as built by its CMake Release flags). */
 int sk_csr_matvec(const sk_csr* m, const double* x_dev, double* y_dev, void* stream);

@@ -99,6 +99,8 @@ class DeviceCsr {
     check(sk_csr_assemble(ds.get(), &d, index_bits, &h, nullptr));
     h_.reset(h);
   }
+  /// adopt a handle returned by the C-ABI (e.g. sk_csr_matmul)
+  explicit DeviceCsr(sk_csr* adopt) { h_.reset(adopt); }
   sk_csr* get() const { return h_.get(); }
   std::int64_t rows() const {
     int64_t r = 0;
@@ -317,6 +319,16 @@ class CahnHilliardStepper {
 
 inline void imex_step(CahnHilliardStepper& stepper, CahnHilliardState& s, double dt, int order) {
   stepper.step(s, dt, order);
+}
+
+/// csr_matmul (linalg.cpp:253-283) on the device: b * a, bit-identical values.
+inline CsrMatrix csr_matmul(const CsrMatrix& b, const CsrMatrix& a) {
+  if (b.cols != a.rows) throw Error(Errc::shape_mismatch, "inner dimensions do not match");
+  const DeviceCsr db(b), da(a);
+  sk_csr* out = nullptr;
+  check(sk_csr_matmul(db.get(), da.get(), &out, nullptr));
+  const DeviceCsr prod(out);
+  return prod.download();
 }
 
 /// power_iteration (linalg.cpp:74-106): the loop runs on the device.

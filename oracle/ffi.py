@@ -79,6 +79,7 @@ class Oracle:
         L.sko_ch_init.argtypes = [C.c_int, i64, dbl, dbl, dbl, vp]
         L.sko_ch_imex_seq.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int, vp, vp, vp, vp]
         L.sko_identity_plus_scaled.argtypes = [C.POINTER(SkoCsr), dbl, C.POINTER(SkoCsr)]
+        L.sko_csr_matmul.argtypes = [C.POINTER(SkoCsr), C.POINTER(SkoCsr), C.POINTER(SkoCsr)]
         L.sko_power_iteration.argtypes = [C.POINTER(SkoCsr), dbl, C.c_uint64, i64, C.POINTER(dbl), C.POINTER(i64)]
         L.sko_periodic_eigen.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, dbl, dbl, dbl, vp, C.POINTER(dbl),
                                          C.POINTER(dbl)]
@@ -190,6 +191,30 @@ class Oracle:
         out = np.empty(n ** dim)
         self.L.sko_ch_init(dim, n, h, c0, eps, _p(out))
         return out
+
+    def csr_matmul(self, b, a):
+        """b, a: (row_ptr, col_idx, values) triples -> the product triple (linalg.cpp:253-283)."""
+        def mk(t, keep):
+            m = SkoCsr()
+            rp, ci, v = (np.ascontiguousarray(t[0], np.int64), np.ascontiguousarray(t[1], np.int64),
+                         np.ascontiguousarray(t[2], np.float64))
+            keep += [rp, ci, v]
+            m.rows = rp.size - 1
+            m.cols = int(ci.max()) + 1 if ci.size else 0
+            m.nnz = ci.size
+            m.row_ptr = rp.ctypes.data_as(C.POINTER(C.c_int64))
+            m.col_idx = ci.ctypes.data_as(C.POINTER(C.c_int64))
+            m.values = v.ctypes.data_as(C.POINTER(C.c_double))
+            return m
+        keep = []
+        mb, ma, out = mk(b, keep), mk(a, keep), SkoCsr()
+        ma.cols = max(ma.cols, ma.rows)
+        self.L.sko_csr_matmul(C.byref(mb), C.byref(ma), C.byref(out))
+        r = np.ctypeslib.as_array(out.row_ptr, shape=(out.rows + 1,)).copy()
+        c = np.ctypeslib.as_array(out.col_idx, shape=(max(out.nnz, 1),))[: out.nnz].copy()
+        v = np.ctypeslib.as_array(out.values, shape=(max(out.nnz, 1),))[: out.nnz].copy()
+        self.L.sko_csr_free(C.byref(out))
+        return r, c, v
 
     def power_iteration(self, rp, ci, vals, tol, seed=20240801, max_iter=2_000_000):
         m = SkoCsr()
@@ -340,6 +365,8 @@ class Reference:
         L.skref_power_iteration.argtypes = [vp, dbl, C.c_ulonglong, C.c_longlong, C.POINTER(dbl)]
         L.skref_periodic_spectrum.argtypes = [C.c_int, C.c_int, C.c_int, vp, dbl, dbl, dbl, vp, C.POINTER(dbl),
                                               C.POINTER(dbl), C.POINTER(dbl)]
+        L.skref_csr_matmul.argtypes = [vp, vp]
+        L.skref_csr_matmul.restype = vp
         L.skref_identity_plus_scaled.argtypes = [vp, dbl]
         L.skref_identity_plus_scaled.restype = vp
         self.L = L

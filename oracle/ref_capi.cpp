@@ -430,6 +430,11 @@ int skref_ch_init(int dim, int n, double h, double c0, double eps_ic, double* ou
   }
 }
 
+// csr_matmul (linalg.cpp:253-283) of two assembled handles: b * a
+void* skref_csr_matmul(void* b, void* a) {
+  return new CsrMatrix(csr_matmul(*static_cast<CsrMatrix*>(b), *static_cast<CsrMatrix*>(a)));
+}
+
 // identity_plus_scaled (linalg.cpp:224-251) on an assembled operator
 void* skref_identity_plus_scaled(void* mp, double alpha) {
   return new CsrMatrix(identity_plus_scaled(*static_cast<CsrMatrix*>(mp), alpha));

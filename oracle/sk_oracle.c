@@ -559,6 +559,58 @@ int sko_ch_imex(int dim, int64_t n, double h, double mobility, double kappa, dou
   return sko_ch_imex_seq(dim, n, h, mobility, kappa, rho_w, c_alpha, c_beta, rel_tol, 1, &dt, &order, &nsteps, c);
 }
 
+/* csr_matmul (linalg.cpp:253-283): out = b * a, dense accumulator per row,
+ * columns recorded on first touch (acc == 0), sorted, exact zeros dropped */
+static int cmp_i64(const void* x, const void* y) {
+  const int64_t a = *(const int64_t*)x, b = *(const int64_t*)y;
+  return (a > b) - (a < b);
+}
+int sko_csr_matmul(const sko_csr* b, const sko_csr* a, sko_csr* out) {
+  out->rows = b->rows;
+  out->cols = a->cols;
+  out->row_ptr = (int64_t*)calloc((size_t)b->rows + 1, sizeof(int64_t));
+  double* acc = (double*)calloc((size_t)(a->cols > 0 ? a->cols : 1), sizeof(double));
+  int64_t cap = 1024, nnz = 0;
+  out->col_idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  out->values = (double*)malloc(sizeof(double) * (size_t)cap);
+  int64_t tcap = 1024;
+  int64_t* touched = (int64_t*)malloc(sizeof(int64_t) * (size_t)tcap);
+  for (int64_t i = 0; i < b->rows; ++i) {
+    int64_t nt = 0;
+    for (int64_t kb = b->row_ptr[i]; kb < b->row_ptr[i + 1]; ++kb) {
+      const int64_t j = b->col_idx[kb];
+      const double vb = b->values[kb];
+      for (int64_t ka = a->row_ptr[j]; ka < a->row_ptr[j + 1]; ++ka) {
+        const int64_t c = a->col_idx[ka];
+        if (acc[c] == 0.0) {
+          if (nt == tcap) touched = (int64_t*)realloc(touched, sizeof(int64_t) * (size_t)(tcap *= 2));
+          touched[nt++] = c;
+        }
+        acc[c] += vb * a->values[ka];
+      }
+    }
+    qsort(touched, (size_t)nt, sizeof(int64_t), cmp_i64);
+    for (int64_t t = 0; t < nt; ++t) {
+      const int64_t c = touched[t];
+      if (acc[c] != 0.0) {
+        if (nnz == cap) {
+          cap *= 2;
+          out->col_idx = (int64_t*)realloc(out->col_idx, sizeof(int64_t) * (size_t)cap);
+          out->values = (double*)realloc(out->values, sizeof(double) * (size_t)cap);
+        }
+        out->col_idx[nnz] = c;
+        out->values[nnz++] = acc[c];
+      }
+      acc[c] = 0.0;
+    }
+    out->row_ptr[i + 1] = nnz;
+  }
+  out->nnz = nnz;
+  free(acc);
+  free(touched);
+  return 0;
+}
+
 /* power_iteration (linalg.cpp:74-106), serial reductions */
 int sko_power_iteration(const sko_csr* m, double tol, uint64_t seed, int64_t max_iter, double* out,
                         int64_t* iterations) {

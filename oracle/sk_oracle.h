@@ -44,6 +44,7 @@ int sko_ch_imex_seq(int dim, int64_t n, double h, double mobility, double kappa,
                     const int64_t* steps, double* c);
 int sko_ch_imex(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
                 double c_beta, double rel_tol, double dt, int order, int64_t nsteps, double* c);
+int sko_csr_matmul(const sko_csr* b, const sko_csr* a, sko_csr* out);
 int sko_power_iteration(const sko_csr* m, double tol, uint64_t seed, int64_t max_iter, double* out,
                         int64_t* iterations);
 void sko_periodic_eigen(int dim, int nent, const int* off, const double* coeff, int h_power, const int64_t* n,

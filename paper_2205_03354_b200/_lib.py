@@ -80,6 +80,7 @@ SIGNATURES = {
     "sk_ch_imex_step": (c_int, [vp, vp, c_dbl, c_int, c_i64, C.POINTER(SolveReportC), C.POINTER(c_i64), vp]),
     "sk_ch_imex_matrix": (c_int, [vp, c_int, C.POINTER(vp)]),
     "sk_ch_init_host": (c_int, [C.POINTER(GridDesc), c_dbl, c_dbl, vp]),
+    "sk_csr_matmul": (c_int, [vp, vp, C.POINTER(vp), vp]),
     "sk_power_iteration": (c_int, [vp, c_dbl, C.c_uint64, c_i64, pd, C.POINTER(c_i64), vp]),
     "sk_periodic_spectrum": (c_int, [vp, C.POINTER(GridDesc), c_dbl, c_dbl, vp, pd, pd, pd]),
     "sk_csr_assemble": (c_int, [vp, C.POINTER(GridDesc), c_int, C.POINTER(vp), vp]),

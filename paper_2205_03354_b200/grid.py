@@ -165,6 +165,15 @@ def assemble(s, g: GridSpec, index_bits: int = 64, stream=None) -> CsrMatrix:
     return CsrMatrix(h.value)
 
 
+def csr_matmul(b: CsrMatrix, a: CsrMatrix, stream=None) -> CsrMatrix:
+    """b * a on the device (linalg.cpp:253-283), bit-identical values."""
+    if b.cols != a.rows:
+        raise StencilkitError(Errc.shape_mismatch, "inner dimensions do not match")
+    h = C.c_void_p()
+    check(b.lib.sk_csr_matmul(b.handle, a.handle, C.byref(h), stream))
+    return CsrMatrix(h.value)
+
+
 def sparsity_report(m: CsrMatrix) -> Tuple[int, float]:
     """(nnz, fill percentage), grid.cpp:160-164."""
     return m.nnz(), 100.0 * float(m.nnz()) / (float(m.rows) * float(m.cols))

@@ -189,6 +189,12 @@ int main() {
     EXPECT(t.symbol_radius == 1.25 && t.spectral_radius == 1.25 && t.condition_estimate == 1.25,
            "time-stepping table row h=4 exact");
   }
+  {  // csr_matmul: bit-identical to the reference's product
+    const GridSpec g = make_periodic_grid(2, 33, 0.25);
+    const CsrMatrix a = assemble(laplacian(2, 4), g), b = assemble(compose(laplacian(2, 2), laplacian(2, 2)), g);
+    const CsrMatrix r = csr_matmul(b, a), c = cuda::csr_matmul(b, a);
+    EXPECT(r.row_ptr == c.row_ptr && r.col_idx == c.col_idx && r.values == c.values, "csr_matmul bit-identical");
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

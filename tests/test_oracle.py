@@ -302,3 +302,20 @@ def test_oracle_spectral_vs_reference(orc, ref):
         assert ref.L.skref_power_iteration(m.h, 1e-8, 20240801, 2_000_000, ctypes.byref(out)) == 0
         lam, its = orc.power_iteration(*m.arrays(), 1e-8)
         assert lam == out.value, (lam, out.value)
+
+
+def test_oracle_csr_matmul_vs_reference(orc, ref):
+    # csr_matmul (linalg.cpp:253-283): the C restatement equals the reference
+    from oracle.ffi import RefCsr
+
+    for dim, acc_a, kind_a, acc_b, kind_b, n, bc in [(2, 2, 1, 2, 2, (9, 8), 0), (3, 2, 2, 2, 1, (6, 6, 7), 0),
+                                                    (2, 4, 1, 2, 1, (12, 11), 1), (1, 2, 2, 4, 2, (17,), 0)]:
+        a = RefCsr(ref, dim, acc_a, kind_a, list(n), 0.5, [bc] * dim)
+        b = RefCsr(ref, dim, acc_b, kind_b, list(n), 0.5, [bc] * dim)
+        out = ref.L.skref_csr_matmul(b.h, a.h)
+        rows, nnz = ref.L.skref_csr_rows(out), ref.L.skref_csr_nnz(out)
+        r2, c2, v2 = np.empty(rows + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+        ref.L.skref_csr_copy(out, r2.ctypes.data, c2.ctypes.data, v2.ctypes.data)
+        ref.L.skref_csr_free(out)
+        r1, c1, v1 = orc.csr_matmul(b.arrays(), a.arrays())
+        assert np.array_equal(r1, r2) and np.array_equal(c1, c2) and np.array_equal(v1, v2)
