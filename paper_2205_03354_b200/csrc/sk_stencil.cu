@@ -145,7 +145,21 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
   static int once = set_smem(kern, T2::SMEM_BYTES);
   if (once != SK_OK) return once;
   dim3 grid(unsigned((a.nx + 63) / 64), unsigned((a.ny + 31) / 32));
-  kern<<<grid, T2::THREADS, T2::SMEM_BYTES, stream>>>(a);
+  // programmatic dependent launch: overlaps this grid's ramp-up (tile loads
+  // and, for Apply, the whole computation) with the predecessor's tail
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(T2::THREADS);
+  cfg.dynamicSmemBytes = T2::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const char* env = getenv("SK_PDL");
+  if (env && env[0] == '0') cfg.numAttrs = 0;
+  SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
   SK_LAUNCH_CHECK("stencil2d_kernel");
   return SK_OK;
 }

@@ -140,6 +140,13 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
     mbar_init(bar, 1);
     fence_mbar_init();
   }
+  // Programmatic dependent launch (launch_2d): the next kernel of the stream
+  // may start its CTAs now; this one waits for its predecessor before the
+  // first access that can conflict with it (CH: reading the field the
+  // predecessor wrote; Apply: overwriting the buffer the one before wrote).
+  // Without the launch attribute both instructions are no-ops.
+  asm volatile("griddepcontrol.launch_dependents;");
+  if constexpr (M == Mode::CahnHilliard) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   load_tile_2d<TX, TY, PX, PY>(tile, bar, a, x0, y0);
 
@@ -203,6 +210,7 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
   }
 
   const int64_t gx = x0 + tx * PX;
+  if constexpr (M == Mode::Apply) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < PY; ++j) {
     const int64_t gy = y0 + ly + j;
