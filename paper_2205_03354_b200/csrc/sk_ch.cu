@@ -159,7 +159,18 @@ static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
   // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
-  chf3d_kernel<C, V, LD, OUT><<<unsigned(grid), C::THREADS, SM::BYTES, stream>>>(a, tm);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = SM::BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap launch with the previous step
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  const char* env = getenv("SK_PDL");
+  cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
+  SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, chf3d_kernel<C, V, LD, OUT>, a, tm));
   SK_LAUNCH_CHECK("chf3d_kernel");
   return SK_OK;
 }

@@ -145,6 +145,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   LoadCursor<C> lc;
   TmaCursor<C> tc;
   int s_load = 0;
+  // programmatic dependent launch: wait for the previous step (which wrote
+  // our input) before the first load; the next step is released at the end
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if constexpr (LD == 0) {
     lc.u = ubeg;
     lc.uend = uend;
@@ -365,6 +368,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       if (kb + 2 < np) step(I0{}, T{}, T{});
     }
   }
+  asm volatile("griddepcontrol.launch_dependents;");
   cp_async_wait_all();
 }
 
