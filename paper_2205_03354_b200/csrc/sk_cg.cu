@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kT = 256;
 enum : int { kRunning = 0, kCheck = 1, kNotPD = 2, kMaxIter = 3 };
+constexpr int kLoopUnroll = 4;  // CG iterations per round of the device-side while loop
 
 struct CgState {
   double rho, pq, alpha, beta, target;
@@ -356,10 +357,13 @@ struct CgPlan {
     if (cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
         cudaSuccess)
       return SK_ERR_CUDA;
-    const int st_ = iteration(x, cap, true, h);
+    // body: kLoopUnroll iterations (no-ops once the status leaves RUNNING),
+    // the last one publishing the loop condition
+    int st_ = SK_OK;
+    for (int k = 0; k < kLoopUnroll && st_ == SK_OK; ++k) st_ = iteration(x, cap, k + 1 == kLoopUnroll, h);
     cudaGraph_t out = nullptr;
     const cudaError_t e = cudaStreamEndCapture(cap, &out);
-    g_launches -= kernels_per_iteration();  // capture does not execute
+    g_launches -= int64_t(kernels_per_iteration()) * kLoopUnroll;  // capture does not execute
     if (st_ != SK_OK || e != cudaSuccess) return SK_ERR_CUDA;
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
       exec = nullptr;
@@ -463,9 +467,10 @@ int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options*
     SK_CUDA_TRY(cudaGraphLaunch(s->exec, stream));
     SK_CUDA_TRY(cudaMemcpyAsync(&h, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
-    // launched kernels: the loop runs one round past the last counted iteration
+    // launched kernels: whole loop bodies up to the round that stopped
+    const int64_t rounds = (h.it - it + kLoopUnroll) / kLoopUnroll;
     g_launches += int64_t(s->kernels_per_iteration()) *
-                  (s->device_loop ? (h.it - it + 1) : int64_t(s->check_every));
+                  (s->device_loop ? rounds * kLoopUnroll : int64_t(s->check_every));
     it = h.it;
     rho = h.rho;
     status = h.status;
@@ -509,15 +514,30 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   if (m->rows != m->cols) return fail(SK_ERR_SHAPE_MISMATCH, "cg_solve needs a square matrix");
   if (rep) *rep = sk_solve_report{0, 0, 0.0, 0.0};
   if (m->rows == 0) return SK_OK;
-  CgOperator op;
-  op.m = m;
-  op.n = m->rows;
-  CgPlan* plan = nullptr;
-  if (int e = cg_plan_create(op, o ? o->check_every : 0, stream, &plan)) return e;
-  const int st = cg_plan_solve(plan, b, x, o, rep, stream);
-  cudaStreamSynchronize(stream);  // the workspace is freed synchronously
-  cg_plan_destroy(plan);
-  return st;
+  // one cached plan per host thread: repeated solves on the same matrix reuse
+  // the workspace and the captured iteration graph (matrix uids are unique)
+  struct Cache {
+    uint64_t uid = 0;
+    int check_every = -1;
+    CgPlan* plan = nullptr;
+    ~Cache() { cg_plan_destroy(plan); }
+  };
+  thread_local Cache cache;
+  const int ce = o ? o->check_every : 0;
+  if (!cache.plan || cache.uid != m->uid || cache.check_every != ce) {
+    if (cache.plan) {
+      cudaDeviceSynchronize();  // the old workspace may still be in use by queued work
+      cg_plan_destroy(cache.plan);
+      cache.plan = nullptr;
+    }
+    CgOperator op;
+    op.m = m;
+    op.n = m->rows;
+    if (int e = cg_plan_create(op, ce, stream, &cache.plan)) return e;
+    cache.uid = m->uid;
+    cache.check_every = ce;
+  }
+  return cg_plan_solve(cache.plan, b, x, o, rep, stream);
 }
 
 }  // namespace sk

@@ -17,6 +17,8 @@
 // 5-step binary search over the warp's 33 row pointers in shared memory.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cstring>
 #include <utility>
@@ -24,6 +26,11 @@
 
 #include "sk_internal.hpp"
 #include "sk_sell.cuh"
+
+uint64_t sk_next_csr_uid() {
+  static std::atomic<uint64_t> next{1};
+  return next.fetch_add(1);
+}
 
 sk_csr::~sk_csr() {
   if (row_ptr) cudaFree(row_ptr);

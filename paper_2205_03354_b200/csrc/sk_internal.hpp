@@ -31,7 +31,10 @@ struct sk_stencil {
 };
 
 // Device-resident CSR (grid.hpp:39-46 layout; int32 columns opt-in).
+uint64_t sk_next_csr_uid();
+
 struct sk_csr {
+  uint64_t uid = sk_next_csr_uid();  // never reused: keys cached solver plans
   int64_t rows = 0, cols = 0, nnz = 0;
   int index_bits = 64;
   int64_t* row_ptr = nullptr;
