@@ -260,6 +260,35 @@ def run_ch(lib, dim: int, steps: int, warmup: int, d: Dist, e2e: bool = True, fo
     return res
 
 
+def _ref_csr_timing(dim: int, acc: int, kind: int, n: int, h: float, bc: int, matvecs: int = 5, cg_iters: int = 0):
+    """The reference's own CPU path on the host cores: assemble (timed) + csr_matvec
+    (+ a bounded cg_solve) on the same operator. Returns a dict for 'reference_cpu'."""
+    try:
+        from oracle.ffi import RefCsr, Reference
+
+        ref = Reference()
+        t0 = time.perf_counter()
+        m = RefCsr(ref, dim, acc, kind, [n] * dim, h, [bc] * dim)
+        asm_s = time.perf_counter() - t0
+        x, y = field(13, m.rows, 1.0), np.empty(m.rows)
+        m.matvec(x, y)
+        t0 = time.perf_counter()
+        for _ in range(matvecs):
+            m.matvec(x, y)
+        mv_s = (time.perf_counter() - t0) / matvecs
+        out = {"cores": ref.threads(), "assembly_ms": asm_s * 1e3, "matvec_ms": mv_s * 1e3, "rows": m.rows,
+               "nnz": m.nnz, "rows_per_s": m.rows / mv_s}
+        if cg_iters:
+            xs = np.zeros(m.rows)
+            t0 = time.perf_counter()
+            m.cg_solve(x, xs, 1e-30, cg_iters)  # runs out of budget by design: a timed iteration sample
+            out["cg_ms_per_iteration"] = (time.perf_counter() - t0) * 1e3 / cg_iters
+        m.close()
+        return out
+    except Exception as ex:  # the reference library only exists where it was built
+        return {"unavailable": repr(ex)}
+
+
 def extra_apply2d(lib):
     """Config 1: 13-point composed biharmonic, 1024^2 periodic, 100 applications (one CUDA graph)."""
     from paper_2205_03354_b200.device import DeviceArray
@@ -284,9 +313,14 @@ def extra_apply2d(lib):
     ms = statistics.median(times)
     pts = reps * n * n
     gbs = 16.0 * pts / (ms * 1e-3) / 1e9
+    rc = _ref_csr_timing(2, 2, 2, n, 1.0 / n, 0, matvecs=10)
+    if "matvec_ms" in rc:
+        rc.update(value=n * n / (rc["matvec_ms"] * 1e-3) / 1e9, unit="Gpts/s",
+                  sample="10 csr_matvec of the reference-assembled 13-pt matrix (the reference has no matrix-free "
+                         "apply); assembly timed separately")
     return {"config": "1: 13-pt apply 1024^2 x100 (graph)", "value": pts / (ms * 1e-3) / 1e9, "unit": "Gpts/s",
             "ms_per_100": ms, "achieved_gbs": gbs, "note": "8.4 MB field: L2-resident across the 100 applications; "
-            "L2 flushed before each timed batch"}
+            "L2 flushed before each timed batch", "reference_cpu": rc}
 
 
 def extra_apply3d(lib, which: str):
@@ -309,8 +343,14 @@ def extra_apply3d(lib, which: str):
         composed_apply(s, g, u, out=v)
     ms = ev.stop_ms() / reps
     pts = n ** 3
+    rc = _ref_csr_timing(3, acc, 2, 128, 1.0 / 128, 0, matvecs=3)
+    if "matvec_ms" in rc:
+        rc.update(value=128 ** 3 / (rc["matvec_ms"] * 1e-3) / 1e9, unit="Gpts/s",
+                  sample="3 csr_matvec of the reference-assembled matrix at 128^3 (256^3 assembly alone needs "
+                         "~20 GB and 20+ s on the host)")
     return {"config": f"{which}-pt composed apply 256^3 periodic", "value": pts / (ms * 1e-3) / 1e9,
-            "unit": "Gpts/s", "ms_per_apply": ms, "achieved_gbs": 16.0 * pts / (ms * 1e-3) / 1e9}
+            "unit": "Gpts/s", "ms_per_apply": ms, "achieved_gbs": 16.0 * pts / (ms * 1e-3) / 1e9,
+            "reference_cpu": rc}
 
 
 def extra_csr73(lib, bits: int):
@@ -341,10 +381,18 @@ def extra_csr73(lib, bits: int):
     spmv_bytes = (8 + idx) * nnz + 8 * (rows + 1) + 16 * rows
     asm_bytes = (8 + idx) * nnz + 8 * (rows + 1)
     del m
-    return {"config": f"5: 73-pt clamped CSR 255^3 (int{bits} cols)", "rows": rows, "nnz": nnz,
-            "assembly_ms": asm_ms, "assembly_gbs_written": asm_bytes / (asm_ms * 1e-3) / 1e9,
-            "spmv_ms": ms, "spmv_grows_per_s": rows / (ms * 1e-3) / 1e9,
-            "spmv_achieved_gbs": spmv_bytes / (ms * 1e-3) / 1e9}
+    out = {"config": f"5: 73-pt clamped CSR 255^3 (int{bits} cols)", "rows": rows, "nnz": nnz,
+           "assembly_ms": asm_ms, "assembly_gbs_written": asm_bytes / (asm_ms * 1e-3) / 1e9,
+           "spmv_ms": ms, "spmv_grows_per_s": rows / (ms * 1e-3) / 1e9,
+           "spmv_achieved_gbs": spmv_bytes / (ms * 1e-3) / 1e9}
+    if bits == 64:
+        rc = _ref_csr_timing(3, 4, 2, 128, 1.0 / 128, 2, matvecs=3)
+        if "matvec_ms" in rc:
+            rc.update(sample="reference assemble + 3 csr_matvec at 128 intervals (127^3 rows; 255^3 needs 38 GB "
+                             "RSS and 22 s for the assembly alone)",
+                      assembly_rows_per_s=rc["rows"] / (rc["assembly_ms"] * 1e-3))
+        out["reference_cpu"] = rc
+    return out
 
 
 def extra_cg(lib, N: int = 1024, iters: int = 256):
@@ -375,8 +423,11 @@ def extra_cg(lib, N: int = 1024, iters: int = 256):
     ms = ev.stop_ms()
     per = ms / max(rep.iterations, 1)
     bytes_it = 16 * m.nnz() + 8 * (m.rows + 1) + 16 * m.rows + 48 * m.rows + 24 * m.rows
+    rc = _ref_csr_timing(2, 2, 2, N + 1, 1.0 / N, 2, matvecs=3, cg_iters=20)
+    if "cg_ms_per_iteration" in rc:
+        rc.update(sample="20 cg_solve iterations of the reference on its own assembled matrix")
     return {"config": f"2: CG 13-pt clamped N={N} ({m.rows} rows)", "iterations": rep.iterations,
-            "ms_per_iteration": per, "achieved_gbs": bytes_it / (per * 1e-3) / 1e9}
+            "ms_per_iteration": per, "achieved_gbs": bytes_it / (per * 1e-3) / 1e9, "reference_cpu": rc}
 
 
 def extra_imex(lib, dim: int = 2, n: int = 1024, steps: int = 10, ref_steps: int = 2):
@@ -558,9 +609,17 @@ def run_ch_2d_extra(lib, dim, args, formulation="factored", same=False):
     other = dim if same else (2 if dim == 3 else 3)
     r = run_ch(lib, other, 200, 5, _NoDist(), e2e=False, formulation=formulation)
     ms = r["ms"] / 200
-    return {"config": f"{3 if other == 2 else 4}: CH {r['n']}^{other} ({formulation} kernel)", "value": 1e3 / ms,
-            "unit": "steps/s", "ms_per_step": ms, "achieved_gbs": 16.0 * r["points"] / (ms * 1e-3) / 1e9,
-            "note": "2 x 33.5 MB fields stay L2-resident" if other == 2 else ""}
+    out = {"config": f"{3 if other == 2 else 4}: CH {r['n']}^{other} ({formulation} kernel)", "value": 1e3 / ms,
+           "unit": "steps/s", "ms_per_step": ms, "achieved_gbs": 16.0 * r["points"] / (ms * 1e-3) / 1e9,
+           "note": "2 x 33.5 MB fields stay L2-resident" if other == 2 else ""}
+    if not same:
+        try:
+            sps, el, setup_s, threads = ref_ch_steps_per_s(other, 3, 1)
+            out["reference_cpu"] = {"value": sps, "unit": "steps/s", "cores": threads,
+                                    "sample": "3 explicit steps from the reference's own L, B matrices"}
+        except Exception as ex:
+            out["reference_cpu"] = {"unavailable": repr(ex)}
+    return out
 
 
 class _NoDist:
