@@ -75,6 +75,7 @@ class Oracle:
         L.sko_cg_solve.argtypes = [C.POINTER(SkoCsr), vp, vp, dbl, i64, C.c_int, C.POINTER(i64), C.POINTER(dbl)]
         L.sko_apply_direct.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, dbl, vp, vp, vp]
         L.sko_ch_explicit.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, vp]
+        L.sko_ch_explicit_dims.argtypes = [C.c_int, vp, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, vp]
         L.sko_ch_imex.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int, i64, vp]
         L.sko_ch_init.argtypes = [C.c_int, i64, dbl, dbl, dbl, vp]
         L.sko_ch_imex_seq.argtypes = [C.c_int, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, C.c_int, vp, vp, vp, vp]
@@ -162,6 +163,16 @@ class Oracle:
         c = np.ascontiguousarray(c, np.float64).ravel().copy()
         st = self.L.sko_ch_explicit(dim, n, h, params.mobility, params.kappa, params.rho_w, params.c_alpha,
                                     params.c_beta, dt, nsteps, _p(c))
+        if st:
+            raise ValueError(f"oracle ch_explicit failed with status {st}")
+        return c
+
+    def ch_explicit_dims(self, dims, h, params, dt, nsteps, c) -> np.ndarray:
+        """explicit CH on a non-cubic periodic grid (dims: points per axis)"""
+        c = np.ascontiguousarray(c, np.float64).ravel().copy()
+        nd = np.ascontiguousarray(list(dims) + [1] * (3 - len(dims)), np.int64)
+        st = self.L.sko_ch_explicit_dims(len(dims), _p(nd), h, params.mobility, params.kappa, params.rho_w,
+                                         params.c_alpha, params.c_beta, dt, nsteps, _p(c))
         if st:
             raise ValueError(f"oracle ch_explicit failed with status {st}")
         return c

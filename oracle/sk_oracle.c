@@ -399,11 +399,18 @@ static double f_chem_prime(double c, double rho_w, double ca, double cb) { /* ca
  * w = f'(c); a = L w; b = B c; c += dt * M * (a - kappa * b). */
 int sko_ch_explicit(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
                     double c_beta, double dt, int64_t nsteps, double* c) {
-  int lo[3 * 7], bo[3 * 49];
+  const int64_t nn[3] = {n, n, n};
+  return sko_ch_explicit_dims(dim, nn, h, mobility, kappa, rho_w, c_alpha, c_beta, dt, nsteps, c);
+}
+
+/* the same on an n[0] x n[1] (x n[2]) periodic grid */
+int sko_ch_explicit_dims(int dim, const int64_t* ndims, double h, double mobility, double kappa, double rho_w,
+                         double c_alpha, double c_beta, double dt, int64_t nsteps, double* c) {
+  int lo[3 * 7] = {0}, bo[3 * 49] = {0};
   double lc[7], bcf[49];
   const int nl = lap_entries(dim, lo, lc);
   const int nb = compose_entries(dim, nl, lo, lc, bo, bcf);
-  const int64_t nn[3] = {n, n, n};
+  const int64_t nn[3] = {ndims[0], dim > 1 ? ndims[1] : 1, dim > 2 ? ndims[2] : 1};
   const int bcs[3] = {0, 0, 0};
   sko_csr L, B;
   int st = sko_assemble(dim, nl, lo, lc, -2, nn, h, bcs, &L);
@@ -484,7 +491,7 @@ int sko_identity_plus_scaled(const sko_csr* m, double alpha, sko_csr* out) {
 int sko_ch_imex_seq(int dim, int64_t n, double h, double mobility, double kappa, double rho_w, double c_alpha,
                     double c_beta, double rel_tol, int nlegs, const double* dts, const int* orders,
                     const int64_t* steps, double* c) {
-  int lo[3 * 7], bo[3 * 49];
+  int lo[3 * 7] = {0}, bo[3 * 49] = {0};
   double lc[7], bcf[49];
   const int nl = lap_entries(dim, lo, lc);
   const int nb = compose_entries(dim, nl, lo, lc, bo, bcf);

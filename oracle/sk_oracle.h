@@ -50,6 +50,8 @@ int sko_power_iteration(const sko_csr* m, double tol, uint64_t seed, int64_t max
 void sko_periodic_eigen(int dim, int nent, const int* off, const double* coeff, int h_power, const int64_t* n,
                         double h, double shift, double scale, double* eig, double* rho_out, double* cond_out);
 void sko_ch_init(int dim, int64_t n, double h, double c0, double eps, double* out);
+int sko_ch_explicit_dims(int dim, const int64_t* n, double h, double mobility, double kappa, double rho_w,
+                         double c_alpha, double c_beta, double dt, int64_t nsteps, double* c);
 double sko_free_energy(int dim, int64_t n, double h, double kappa, double rho_w, double c_alpha, double c_beta,
                        const double* c);
 void sko_biharmonic_clamped(int dim, int64_t intervals, double* f, double* u_exact);

@@ -344,3 +344,41 @@ def test_cg_biharmonic_clamped_vs_oracle(orc, dim, acc, intervals, tol):
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= 1e-8
     assert rep.true_rel_residual <= tol
     assert abs(rep.iterations - iters) <= max(5, iters // 20)
+
+
+@pytest.mark.parametrize("dims,steps", [((64, 32, 5), 100), ((128, 64, 6), 230), ((96, 40, 7), 120), ((64, 32, 9), 100),
+                                        ((128, 48), 150)])
+def test_ch_noncubic_grids(orc, dims, steps, monkeypatch):
+    # non-cubic periodic grids, tiny z extents (z wrap inside one chunk), the
+    # ghost-padded TMA path (whole tiles) and the plain path, vs the oracle
+    from paper_2205_03354_b200.grid import GridSpec
+
+    dim = len(dims)
+    p = CahnHilliardParams.from_epsilon(0.02)
+    h = 1.0 / max(dims)
+    dt = 0.2 * h ** 4 / (144 * p.kappa)
+    g = GridSpec(dim=dim, n=list(dims), h=h, origin=[0.0] * dim, bc=[BoundaryKind.periodic] * dim)
+    c0 = 0.05 * uniform(6, g.unknown_count())
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SK_CH_PADDED", flag)
+        st = CahnHilliardState(g, c0.copy())
+        CahnHilliardExplicit(g, p).step(st, dt, steps)
+        out[flag] = st.c.copy()
+    assert np.array_equal(out["1"], out["0"])
+    ref = orc.ch_explicit_dims(dims, h, p, dt, steps, c0)
+    assert np.linalg.norm(out["1"] - ref) / np.linalg.norm(ref) <= 1e-9
+
+
+def test_ch_rejects_narrow_axes():
+    # the 25-point B needs 5 points per periodic axis (grid.cpp:66-75), and every
+    # grid at least 3 points per axis (grid.cpp:17-25)
+    from paper_2205_03354_b200.grid import GridSpec
+
+    p = CahnHilliardParams.from_epsilon(0.02)
+    for dims, code in [((64, 32, 4), Errc.stencil_wider_than_grid), ((64, 32, 2), Errc.invalid_argument)]:
+        g = GridSpec(dim=3, n=list(dims), h=0.1, origin=[0.0] * 3, bc=[BoundaryKind.periodic] * 3)
+        with pytest.raises(StencilkitError) as e:
+            st = CahnHilliardState(g, np.zeros(int(np.prod(dims))))
+            CahnHilliardExplicit(g, p).step(st, 1e-9, 1)
+        assert e.value.code == code
