@@ -169,9 +169,9 @@ int launch_3d(Args3D a, cudaStream_t stream) {
   auto kern = stream3d_kernel<M, C>;
   static int once = set_smem(kern, C::SMEM_BYTES);
   if (once != SK_OK) return once;
-  // lockstep for the radius-2 kernels (halo rows from L2), balanced for the
-  // issue-bound radius-4 kernel (measured at 256^3)
-  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/C::R == 2);
+  // lockstep for the radius-2 apply (halo rows from L2), balanced for the
+  // issue-bound radius-4 apply and the composed CH step (measured at 256^3)
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/C::R == 2 && M == Mode::Apply);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   kern<<<unsigned(grid), C::THREADS, C::SMEM_BYTES, stream>>>(a);
   SK_LAUNCH_CHECK("stream3d_kernel");

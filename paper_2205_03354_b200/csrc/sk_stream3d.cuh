@@ -324,8 +324,18 @@ __device__ __forceinline__ void plane_slices(const double* base, const Args3D& a
     }
 }
 
-using Cfg3R2 = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 25-point apply
-using Cfg3CH = Cfg3<2, 64, 16, 2, 2, 8, 2>;    // 3D CH (7-point L f' + 25-point B)
+#ifndef SK_A25_TY
+#define SK_A25_TY 16
+#define SK_A25_S 8
+#define SK_A25_MINB 2
+#endif
+using Cfg3R2 = Cfg3<2, 64, SK_A25_TY, 2, 2, SK_A25_S, SK_A25_MINB>;    // 25-point apply
+#ifndef SK_CH3_TY  // experiments: -DSK_CH3_TY=.. -DSK_CH3_S=.. -DSK_CH3_MINB=..
+#define SK_CH3_TY 16
+#define SK_CH3_S 8
+#define SK_CH3_MINB 1  // 1 CTA/SM: 194 registers, no spills (2 CTAs/SM spilled: 96 -> 82 us at 256^3)
+#endif
+using Cfg3CH = Cfg3<2, 64, SK_CH3_TY, 2, 2, SK_CH3_S, SK_CH3_MINB>;    // 3D CH (7-point L f' + 25-point B)
 using Cfg3R4 = Cfg3<4, 64, 16, 2, 2, 8, 1>;    // 73-point apply
 using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
 using CfgChf3T = Cfg3<2, 64, 32, 2, 2, 8, 1>;  // factored 3D CH, TMA loads from ghost-padded fields
