@@ -336,7 +336,13 @@ using Cfg3R2 = Cfg3<2, 64, SK_A25_TY, 2, 2, SK_A25_S, SK_A25_MINB>;    // 25-poi
 #define SK_CH3_MINB 1  // 1 CTA/SM: 194 registers, no spills (2 CTAs/SM spilled: 96 -> 82 us at 256^3)
 #endif
 using Cfg3CH = Cfg3<2, 64, SK_CH3_TY, 2, 2, SK_CH3_S, SK_CH3_MINB>;    // 3D CH (7-point L f' + 25-point B)
-using Cfg3R4 = Cfg3<4, 64, 16, 2, 2, 8, 1>;    // 73-point apply
+#ifndef SK_A73_TY
+#define SK_A73_TY 16
+#define SK_A73_PX 2
+#define SK_A73_S 8
+#define SK_A73_MINB 1
+#endif
+using Cfg3R4 = Cfg3<4, 64, SK_A73_TY, SK_A73_PX, 2, SK_A73_S, SK_A73_MINB>;    // 73-point apply
 using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
 using CfgChf3T = Cfg3<2, 64, 32, 2, 2, 8, 1>;  // factored 3D CH, TMA loads from ghost-padded fields
 
