@@ -91,3 +91,21 @@ def test_config5_assembly_sampled_rows_at_257(orc):
         cols, vals = orc.assemble_row(s, g, int(r))
         assert rp[r + 1] - rp[r] == cols.size
     assert rp[-1] == m.nnz()
+
+
+@pytest.mark.parametrize("dim,n,steps", [(2, 512, 10000), (3, 128, 2000)])
+def test_config_step_counts_vs_oracle(orc, dim, n, steps):
+    """The configs' full step counts (10,000 in 2D, 2,000 in 3D) at grids the
+    oracle finishes in seconds, the configs' eps / dt rule and seeds: the
+    accumulated error stays within the 1e-9 bar (both 3D paths are exercised:
+    graph chunks through the ghost-padded TMA kernel)."""
+    _, eps, frac, lw, seed = CFG[dim]
+    h = 1.0 / n
+    p = CahnHilliardParams.from_epsilon(eps)
+    dt = frac * h ** 4 / (lw * eps * eps)
+    g = make_periodic_grid(dim, n, h)
+    c0 = 0.05 * uniform(seed, g.unknown_count())
+    st = CahnHilliardState(g, c0.copy())
+    CahnHilliardExplicit(g, p).step(st, dt, steps)
+    ref = orc.ch_explicit(dim, n, h, p, dt, steps, c0)
+    assert np.linalg.norm(st.c - ref) <= 1e-9 * np.linalg.norm(ref)
