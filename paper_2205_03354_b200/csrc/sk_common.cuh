@@ -199,6 +199,33 @@ __device__ __forceinline__ double reduce_partials(const double* partials, int co
   return block_sum<THREADS>(v, sh);
 }
 
+// Extended unknown index i along an axis with `un` unknowns -> the unknown it
+// reads and a factor (assemble's boundary handling, grid.cpp:104-120):
+// periodic wraps; simply supported reflects oddly about the boundary point
+// (factor -1), clamped evenly (factor +1); the boundary points themselves are
+// zero (factor 0). Indices beyond one reflection (partial-tile padding,
+// never an output's neighbour) read as zero.
+__device__ __forceinline__ int64_t bc_map(int64_t i, int64_t un, int bc, double& factor) {
+  if (i >= 0 && i < un) return i;
+  if (bc == SK_BC_PERIODIC) {
+    i %= un;
+    return i < 0 ? i + un : i;
+  }
+  int64_t gi = i + 1;  // grid index; boundary points 0 and un + 1
+  const int64_t last = un + 1;
+  if (gi == 0 || gi == last) {
+    factor = 0.0;
+    return 0;
+  }
+  gi = gi < 0 ? -gi : 2 * last - gi;
+  if (gi < 1 || gi > un) {  // beyond one reflection: only partial-tile padding reads it
+    factor = 0.0;
+    return 0;
+  }
+  if (bc == SK_BC_SIMPLY_SUPPORTED) factor = -factor;
+  return gi - 1;
+}
+
 __device__ __forceinline__ int64_t wrap_idx(int64_t i, int64_t n) {
   i %= n;
   return i < 0 ? i + n : i;

@@ -211,34 +211,47 @@ static bool all_periodic(const GridInfo& g) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// The streaming kernels need every axis at least as wide as the stencil
+// reach on both sides (periodic wrap / one reflection per side).
+static bool streamable(const sk_stencil* s, const GridInfo& g, int radius) {
+  for (int a = 0; a < g.dim; ++a)
+    if (g.un[a] < 2 * radius + 1) return false;
+  (void)s;
+  return true;
+}
+
 int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream) {
   const double scale = pow_int(g.h, s->h_power);
   OrbitW w{};
   for (int i = 0; i < 8; ++i) w.w[i] = s->orbit_coeff[i] * scale;  // == coeff.to_double()*pow_int (grid.cpp:80)
-  if (s->kclass == 1 && g.dim == 2 && all_periodic(g)) {
+  const bool per = all_periodic(g);
+  if (s->kclass == 1 && g.dim == 2 && streamable(s, g, 2)) {
     Apply2DArgs a{};
     a.u = u;
     a.v = v;
-    a.nx = g.n[0];
-    a.ny = g.n[1];
+    a.nx = g.un[0];
+    a.ny = g.un[1];
     a.w = w;
-    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= 64 + 4 && a.ny >= 32 + 4 && aligned16(u) && aligned16(v);
+    a.bc[0] = g.bc[0];
+    a.bc[1] = g.bc[1];
+    a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= 64 + 4 && a.ny >= 32 + 4 && aligned16(u) && aligned16(v);
     return launch_2d<Mode::Apply>(a, stream);
   }
-  if ((s->kclass == 2 || s->kclass == 3) && g.dim == 3 && all_periodic(g)) {
+  if ((s->kclass == 2 || s->kclass == 3) && g.dim == 3 && streamable(s, g, s->kclass == 2 ? 2 : 4)) {
     Args3D a{};
     a.u = u;
     a.v = v;
-    a.nx = g.n[0];
-    a.ny = g.n[1];
-    a.nz = g.n[2];
+    a.nx = g.un[0];
+    a.ny = g.un[1];
+    a.nz = g.un[2];
+    for (int i = 0; i < 3; ++i) a.bc[i] = g.bc[i];
     for (int i = 0; i < 8; ++i) a.w[i] = w.w[i];
     if (s->kclass == 2) {
-      a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R &&
+      a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R &&
                   aligned16(u) && aligned16(v);
       return launch_3d<Mode::Apply, C3R2>(a, stream);
     }
-    a.bulk_ok = (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
+    a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
                 aligned16(u) && aligned16(v);
     return launch_3d<Mode::Apply, C3R4>(a, stream);
   }

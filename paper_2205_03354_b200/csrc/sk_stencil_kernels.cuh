@@ -96,7 +96,8 @@ struct Apply2DArgs {
   OrbitW w;      // scaled orbit weights of the composed stencil (Apply) or B' (CH)
   double wl0, wl1;  // CH: scaled 5-point Laplacian weights (center, axis)
   Poly3 chem;
-  int bulk_ok;   // 1: nx even and >= TX+4 -> TMA bulk row copies
+  int bulk_ok;   // 1: nx even and >= TX+4, periodic -> 16-byte cp.async rows
+  int bc[2];     // boundary kind per axis (nx, ny are unknown counts)
 };
 
 template <int TX, int TY, int PX, int PY>
@@ -117,10 +118,11 @@ __device__ __forceinline__ void load_tile_2d(double* tile, uint64_t* bar, const 
     cp_async_wait_all();
     __syncthreads();
   } else {
-    for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {
+    for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {  // any boundary kind
       const int r = i / T::PITCH, c = i % T::PITCH;
-      const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
-      tile[i] = __ldg(a.u + gy * a.nx + gx);
+      double f = 1.0;
+      const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
+      tile[i] = f == 0.0 ? 0.0 : f * __ldg(a.u + gy * a.nx + gx);
     }
     __syncthreads();
   }

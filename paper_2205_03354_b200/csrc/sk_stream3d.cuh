@@ -68,6 +68,7 @@ struct Args3D {
   double kl0, kl1;   // factored CH: 7-point Laplacian pre-scaled by -kappa (mu = f' - kappa L c)
   Poly3 chem;        // CH: f'
   int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
+  int bc[3];         // boundary kind per axis (nx, ny, nz are unknown counts); bulk path: periodic only
   int zchunk;        // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
 };
 
@@ -192,7 +193,7 @@ struct PlaneLoader {
 
   // load plane `plane` (z = gz) into stage `stage`, then step to the next
   // plane (back to z = 0 after the last one: periodic z)
-  __device__ __forceinline__ void issue(double* ring, int stage, const Args3D& a, int gz) {
+  __device__ __forceinline__ void issue(double* ring, int stage, const Args3D& a, int gz, int gze) {
     constexpr int R = C::R;
     if (a.bulk_ok) {
       const uint32_t soff = uint32_t(stage) * (C::PLANE * 8);
@@ -201,12 +202,20 @@ struct PlaneLoader {
         if (used(k))
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst[k] + soff), "l"(plane + off[k])
                        : "memory");
-    } else {  // fallback: 8-byte copies, modulo wrap (odd nx, tiny or unaligned grids)
+    } else {  // fallback: 8-byte copies, any boundary kind (odd nx, tiny, unaligned or non-periodic grids)
       double* buf = ring + stage * C::PLANE;
+      double fz = 1.0;
+      const int64_t pz = bc_map(gze, a.nz, a.bc[2], fz);  // gze: the unwrapped plane index
+      const double* src = a.u + pz * a.nx * a.ny;
       for (int i = threadIdx.x; i < C::ROWS * C::WIDTH; i += C::THREADS) {
         const int r = i / C::WIDTH, c = i - r * C::WIDTH;
-        const int64_t gy = wrap_idx(y0 - R + r, a.ny), gx = wrap_idx(x0 - R + c, a.nx);
-        cp_async8(buf + r * C::PITCH + c, plane + gy * a.nx + gx);
+        double f = fz;
+        const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
+        double* d = buf + r * C::PITCH + c;
+        if (f == 1.0)
+          cp_async8(d, src + gy * a.nx + gx);
+        else
+          *d = f == 0.0 ? 0.0 : f * __ldg(src + gy * a.nx + gx);  // boundary zero / odd reflection
       }
     }
     plane = gz + 1 == a.nz ? a.u : plane + a.nx * a.ny;
@@ -351,19 +360,21 @@ using CfgChf3T = Cfg3<2, 64, 32, 2, 2, 8, 1>;  // factored 3D CH, TMA loads from
 // offsets) is out of line so the unrolled plane loop stays lean.
 template <class C>
 struct LoadCursor {
-  int u, uend, lz, lp, np;
+  int u, uend, lz, lze, lp, np;  // lz: wrapped plane index, lze: unwrapped (non-periodic z)
   PlaneLoader<C> ld;
   __device__ __forceinline__ void start(const Args3D& a, const double* ring) {
     const Seg seg = seg_of<C>(a, u, uend);
-    lz = seg.z0 - C::R < 0 ? seg.z0 - C::R + int(a.nz) : seg.z0 - C::R;
+    lze = seg.z0 - C::R;
+    lz = lze < 0 ? lze + int(a.nz) : lze;
     ld.setup(a, ring, seg.x0, seg.y0, lz);
     lp = 0;
     np = seg.len + 2 * C::R;
   }
   __device__ __forceinline__ void issue_next(double* ring, int stage, const Args3D& a) {
     if (u < uend) {
-      ld.issue(ring, stage, a, lz);
+      ld.issue(ring, stage, a, lz, lze);
       lz = lz + 1 == a.nz ? 0 : lz + 1;
+      ++lze;
       if (++lp == np) {
         u += np - 2 * C::R;
         if (u < uend) start(a, ring);
