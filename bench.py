@@ -430,6 +430,42 @@ def extra_cg(lib, N: int = 1024, iters: int = 256):
             "ms_per_iteration": per, "achieved_gbs": bytes_it / (per * 1e-3) / 1e9, "reference_cpu": rc}
 
 
+def extra_cg_matrix_free(lib, dim: int, acc: int, N: int, iters: int):
+    """Configs 2 / 5 CG with the matrix-free operator (stencil apply on the clamped grid,
+    no matrix stream): a fixed number of device iterations."""
+    from paper_2205_03354_b200.device import DeviceArray
+    from paper_2205_03354_b200.errors import StencilkitError
+    from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, make_grid
+    from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve_stencil
+    from paper_2205_03354_b200.stencil import bilaplacian
+
+    g = make_grid(dim, N + 1, 1.0 / N, BoundaryKind.clamped)
+    s = DeviceStencil(bilaplacian(dim, acc))
+    rows = g.unknown_count()
+    b = DeviceArray.from_host(field(3, rows, 1.0))
+    x = DeviceArray(rows)
+    opts = SolveOptions(rel_tol=1e-30, max_iter=iters)
+    for _ in range(2):
+        try:
+            cg_solve_stencil(s, g, b, opts, x_out=x)
+        except StencilkitError:
+            pass
+    ev = Events(lib)
+    rep = SolveReport()
+    ev.start()
+    try:
+        cg_solve_stencil(s, g, b, opts, rep, x_out=x)
+    except StencilkitError:
+        pass
+    per = ev.stop_ms() / max(rep.iterations, 1)
+    bytes_it = 104 * rows  # apply 16 + p.q 16 + x,r update 48 + p update 24 B/row
+    npts = 13 if dim == 2 else 73
+    return {"config": f"{2 if dim == 2 else 5}: matrix-free CG {npts}-pt clamped N={N} ({rows} rows)",
+            "iterations": rep.iterations, "ms_per_iteration": per, "achieved_gbs": bytes_it / (per * 1e-3) / 1e9,
+            "note": "sk_cg_solve_stencil: operator = composed stencil on the clamped grid (no matrix stream); "
+                    "roofline bytes = vectors only (104 B/row/iteration)"}
+
+
 def extra_imex(lib, dim: int = 2, n: int = 1024, steps: int = 10, ref_steps: int = 2):
     """The reference's own CH path (IMEX, CahnHilliardStepper, order 2 = CN/AB2) on
     the device vs the compiled reference on the host cores; reference benchmark
@@ -577,6 +613,7 @@ def main() -> int:
                    lambda: run_ch_2d_extra(lib, dim, args, "composed", same=True),
                    lambda: extra_apply3d(lib, "25"), lambda: extra_apply3d(lib, "73"),
                    lambda: extra_csr73(lib, 64), lambda: extra_csr73(lib, 32), lambda: extra_cg(lib),
+                   lambda: extra_cg_matrix_free(lib, 2, 2, 1024, 256), lambda: extra_cg_matrix_free(lib, 3, 4, 256, 64),
                    lambda: extra_imex(lib, 2, 1024), lambda: extra_imex(lib, 3, 128, ref_steps=1)):
             try:
                 e = fn()

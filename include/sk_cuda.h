@@ -255,6 +255,12 @@ int sk_cg_solve(const sk_csr* m, const double* b_dev, double* x_dev, const sk_so
                 sk_solve_report* report, void* stream);
 int sk_cg_solve_host(const sk_csr* m, const double* b_host, double* x_host,
                      const sk_solve_options* opts, sk_solve_report* report);
+/* Matrix-free CG (no reference symbol): the operator is the composed stencil
+ * on the grid (any boundary kind), i.e. assemble(s, g) without the matrix;
+ * same control flow and contract as sk_cg_solve. Results agree with the CSR
+ * solve to the solver tolerance (products summed in orbit order). */
+int sk_cg_solve_stencil(const sk_stencil* s, const sk_grid_desc* g, const double* b_dev, double* x_dev,
+                        const sk_solve_options* opts, sk_solve_report* report, void* stream);
 
 #ifdef __cplusplus
 }

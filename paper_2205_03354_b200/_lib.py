@@ -98,6 +98,8 @@ SIGNATURES = {
     "sk_xpby": (c_int, [c_i64, vp, c_dbl, vp, vp]),
     "sk_cg_solve": (c_int, [vp, vp, vp, C.POINTER(SolveOptionsC), C.POINTER(SolveReportC), vp]),
     "sk_cg_solve_host": (c_int, [vp, vp, vp, C.POINTER(SolveOptionsC), C.POINTER(SolveReportC)]),
+    "sk_cg_solve_stencil": (c_int, [vp, C.POINTER(GridDesc), vp, vp, C.POINTER(SolveOptionsC), C.POINTER(SolveReportC),
+                                    vp]),
 }
 
 _lib: Optional[C.CDLL] = None

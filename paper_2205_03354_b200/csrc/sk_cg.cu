@@ -540,11 +540,58 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   return cg_plan_solve(cache.plan, b, x, o, rep, stream);
 }
 
+// Matrix-free CG: the operator is the composed stencil applied by the
+// streaming kernels on the grid's boundary kind (equal to assemble(s, g) in
+// exact arithmetic; per-row sums in orbit order instead of column order).
+int cg_solve_stencil(const sk_stencil* s, const GridInfo& g, const double* b, double* x, const sk_solve_options* o,
+                     sk_solve_report* rep, cudaStream_t stream) {
+  if (rep) *rep = sk_solve_report{0, 0, 0.0, 0.0};
+  if (g.rows == 0) return SK_OK;
+  struct Cache {
+    uint64_t uid = 0;
+    GridInfo g{};
+    int check_every = -1;
+    CgPlan* plan = nullptr;
+    ~Cache() { cg_plan_destroy(plan); }
+  };
+  thread_local Cache cache;
+  const int ce = o ? o->check_every : 0;
+  bool hit = cache.plan && cache.uid == s->uid && cache.check_every == ce && cache.g.dim == g.dim && cache.g.h == g.h;
+  for (int a = 0; a < 3 && hit; ++a) hit = cache.g.n[a] == g.n[a] && cache.g.bc[a] == g.bc[a];
+  if (!hit) {
+    if (cache.plan) {
+      cudaDeviceSynchronize();
+      cg_plan_destroy(cache.plan);
+      cache.plan = nullptr;
+    }
+    CgOperator op;
+    op.s = s;
+    op.g = g;
+    op.n = g.rows;
+    if (int e = cg_plan_create(op, ce, stream, &cache.plan)) return e;
+    cache.uid = s->uid;
+    cache.g = g;
+    cache.check_every = ce;
+  }
+  return cg_plan_solve(cache.plan, b, x, o, rep, stream);
+}
+
 }  // namespace sk
 
 using namespace sk;
 
 extern "C" {
+
+int sk_cg_solve_stencil(const sk_stencil* s, const sk_grid_desc* gd, const double* b, double* x,
+                        const sk_solve_options* o, sk_solve_report* rep, void* stream) {
+  if (!s) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (s->dim != g.dim) return fail(SK_ERR_DIM_MISMATCH, "stencil/grid dimension mismatch");
+  if (int st = check_width(s, g)) return st;
+  if (g.rows > 0 && (!b || !x)) return fail(SK_ERR_INVALID_ARGUMENT, "null vector");
+  return cg_solve_stencil(s, g, b, x, o, rep, as_stream(stream));
+}
 
 int sk_cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options* o, sk_solve_report* rep,
                 void* stream) {

@@ -11,7 +11,10 @@
 // Device-ready stencil: the host composition result in canonical order
 // (std::map<Offset, Rational> order, stencil.hpp:44-57), plus its
 // classification onto one of the specialised symmetric kernels.
+uint64_t sk_next_csr_uid();  // unique object ids (never reused) keying cached solver plans
+
 struct sk_stencil {
+  uint64_t uid = sk_next_csr_uid();
   int dim = 0;
   int nent = 0;
   int h_power = 0;
@@ -31,8 +34,6 @@ struct sk_stencil {
 };
 
 // Device-resident CSR (grid.hpp:39-46 layout; int32 columns opt-in).
-uint64_t sk_next_csr_uid();
-
 struct sk_csr {
   uint64_t uid = sk_next_csr_uid();  // never reused: keys cached solver plans
   int64_t rows = 0, cols = 0, nnz = 0;

@@ -74,6 +74,33 @@ def cg_solve(m: CsrMatrix, b, opts: SolveOptions | None = None, report: SolveRep
             report.recurrence_rel_residual = rep.recurrence_rel_residual
 
 
+def cg_solve_stencil(stencil, grid, b, opts: SolveOptions | None = None, report: SolveReport | None = None,
+                     x_out: DeviceArray | None = None, stream=None):
+    """Matrix-free CG on the composed stencil's operator over `grid` (assemble(s, g)
+    without the matrix); same contract as cg_solve. Host b -> host x; DeviceArray b
+    -> DeviceArray x."""
+    from .grid import as_device_stencil
+
+    opts = opts or SolveOptions()
+    ds = as_device_stencil(stencil)
+    d = grid.desc()
+    rows = grid.unknown_count()
+    rep = SolveReportC()
+    o = _opts(opts)
+    host = not isinstance(b, DeviceArray)
+    bd = DeviceArray.from_host(np.ascontiguousarray(np.asarray(b, np.float64).ravel())) if host else b
+    if bd.count != rows:
+        raise StencilkitError(Errc.shape_mismatch, "rhs length does not match the grid")
+    x = x_out if x_out is not None else DeviceArray(rows)
+    try:
+        check(ds.lib.sk_cg_solve_stencil(ds.handle, C.byref(d), bd.ptr, x.ptr, C.byref(o), C.byref(rep), stream))
+    finally:
+        if report is not None:
+            report.iterations, report.restarts = rep.iterations, rep.restarts
+            report.true_rel_residual, report.recurrence_rel_residual = rep.true_rel_residual, rep.recurrence_rel_residual
+    return x.to_host() if host else x
+
+
 # ------------------------------------------------------------ spectral --
 def power_iteration(m: CsrMatrix, tol: float, seed: int = 20240801, max_iter: int = 2_000_000,
                     stream=None) -> float:
