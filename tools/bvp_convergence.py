@@ -36,7 +36,7 @@ from paper_2205_03354_b200 import _lib  # noqa: E402
 from paper_2205_03354_b200.device import DeviceArray  # noqa: E402
 from paper_2205_03354_b200.errors import StencilkitError  # noqa: E402
 from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, assemble, make_grid  # noqa: E402
-from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve  # noqa: E402
+from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve, cg_solve_stencil  # noqa: E402
 from paper_2205_03354_b200.stencil import bilaplacian  # noqa: E402
 
 
@@ -105,6 +105,8 @@ def main() -> None:
     ap.add_argument("--nested", action="store_true")
     ap.add_argument("--max-iter", type=int, default=0)
     ap.add_argument("--index-bits", type=int, default=64)
+    ap.add_argument("--matrix-free", action="store_true",
+                    help="CG on the stencil operator (sk_cg_solve_stencil) instead of the assembled CSR")
     args = ap.parse_args()
     lib = _lib.ensure_device(0)
     s = DeviceStencil(bilaplacian(args.dim, args.acc))
@@ -112,11 +114,12 @@ def main() -> None:
     for N in args.ladder:
         g = make_grid(args.dim, N + 1, 1.0 / N, BoundaryKind.clamped)
         t0 = time.perf_counter()
-        m = assemble(s, g, index_bits=args.index_bits)
+        m = None if args.matrix_free else assemble(s, g, index_bits=args.index_bits)
         t_asm = time.perf_counter() - t0
+        rows = g.unknown_count()
         f, u = manufactured(args.dim, N)
         b = DeviceArray.from_host(f)
-        x = DeviceArray(m.rows)
+        x = DeviceArray(rows)
         use_x0 = args.nested and prev is not None and prev[0] * 2 == N
         if use_x0:
             x.upload(refine(prev[1], args.dim, prev[0]))
@@ -126,7 +129,10 @@ def main() -> None:
         status = "ok"
         t0 = time.perf_counter()
         try:
-            cg_solve(m, b, opts, rep, x_out=x)
+            if m is None:
+                cg_solve_stencil(s, g, b, opts, rep, x_out=x)
+            else:
+                cg_solve(m, b, opts, rep, x_out=x)
         except StencilkitError as e:
             status = str(e)
         t_cg = time.perf_counter() - t0
@@ -134,7 +140,8 @@ def main() -> None:
         err = float(np.abs(xh - u).max())
         samples.append((1.0 / N, err))
         prev = (N, xh)
-        print(json.dumps({"dim": args.dim, "acc": args.acc, "N": N, "rows": m.rows, "nnz": m.nnz(),
+        print(json.dumps({"dim": args.dim, "acc": args.acc, "N": N, "rows": rows, "nnz": m.nnz() if m else None,
+                          "matrix_free": m is None,
                           "assembly_s": round(t_asm, 4), "cg_s": round(t_cg, 3), "iterations": rep.iterations,
                           "ms_per_iteration": round(1e3 * t_cg / max(rep.iterations, 1), 4),
                           "true_rel_residual": rep.true_rel_residual,
