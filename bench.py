@@ -646,7 +646,9 @@ def run_ch_2d_extra(lib, dim, args, formulation="factored", same=False):
     other = dim if same else (2 if dim == 3 else 3)
     r = run_ch(lib, other, 200, 5, _NoDist(), e2e=False, formulation=formulation)
     ms = r["ms"] / 200
-    out = {"config": f"{3 if other == 2 else 4}: CH {r['n']}^{other} ({formulation} kernel)", "value": 1e3 / ms,
+    kname = ("composed 13-pt B + 5-pt L kernel (2D uses it for both formulations: a factored 2D kernel measured "
+             "14.8 vs 13.2 us)") if other == 2 else f"{formulation} kernel"
+    out = {"config": f"{3 if other == 2 else 4}: CH {r['n']}^{other} ({kname})", "value": 1e3 / ms,
            "unit": "steps/s", "ms_per_step": ms, "achieved_gbs": 16.0 * r["points"] / (ms * 1e-3) / 1e9,
            "note": "2 x 33.5 MB fields stay L2-resident" if other == 2 else ""}
     if not same:

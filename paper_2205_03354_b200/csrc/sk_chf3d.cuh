@@ -38,9 +38,6 @@
 
 namespace sk {
 
-// plain 128-bit shared load: unlike the volatile-asm lds128 the compiler may
-// hoist it across independent work
-__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
 // Ghost-padded field of the TMA path: row pitch nx + 2 kPadL, kPadT ghost
 // rows above and below; interior x at column x + kPadL (128 B-aligned rows

@@ -199,6 +199,10 @@ __device__ __forceinline__ double reduce_partials(const double* partials, int co
   return block_sum<THREADS>(v, sh);
 }
 
+// plain 128-bit shared load: unlike a volatile-asm ld.shared the compiler may
+// hoist it across independent work
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
 // Extended unknown index i along an axis with `un` unknowns -> the unknown it
 // reads and a factor (assemble's boundary handling, grid.cpp:104-120):
 // periodic wraps; simply supported reflects oddly about the boundary point
