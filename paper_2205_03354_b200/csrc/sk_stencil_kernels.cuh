@@ -15,11 +15,13 @@
 // op count per point is ~13 (2D 13-pt), ~21 (3D 25-pt), ~49 (3D 73-pt)
 // instead of one FMA per stencil entry.
 //
-// Data movement: tiles (+ radius-R halo) land in shared memory through the
-// TMA bulk-copy engine (cp.async.bulk, SASS UBLKCP) one row segment per copy,
-// periodic wrap handled by splitting a row into <= 2 contiguous pieces, with
-// mbarrier transaction counts. 3D kernels run a warp-specialised ring: one
-// producer warp streams planes ahead of 8 consumer warps.
+// Data movement: tiles (+ radius-R halo) land in shared memory through
+// all-thread 16-byte cp.async (LDGSTS) on periodic grids with aligned rows;
+// otherwise (odd widths, non-periodic boundaries) element-wise with the
+// boundary map of assemble (bc_map: wrap, even / odd reflection, zero
+// boundary points). The 3D kernels (sk_stream3d.cuh) stream planes through a
+// multistage shared ring with one barrier per plane; the headline factored
+// CH kernel (sk_chf3d.cuh) uses TMA boxes from ghost-padded fields.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -101,12 +103,10 @@ struct Apply2DArgs {
 };
 
 template <int TX, int TY, int PX, int PY>
-__device__ __forceinline__ void load_tile_2d(double* tile, uint64_t* bar, const Apply2DArgs& a, int64_t x0,
-                                             int64_t y0) {
+__device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a, int64_t x0, int64_t y0) {
   using T = Tile2D<TX, TY, PX, PY>;
   constexpr int R = T::R;
   const int tid = threadIdx.x;
-  (void)bar;
   if (a.bulk_ok) {
     // every thread issues 16-byte cp.async (LDGSTS) pairs of the haloed tile
     constexpr int HP = T::PITCH / 2;
@@ -134,14 +134,9 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
   using T = Tile2D<TX, TY, PX, PY>;
   constexpr int R = T::R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   double* tile = reinterpret_cast<double*>(smem_raw + 16);
 
   const int64_t x0 = int64_t(blockIdx.x) * TX, y0 = int64_t(blockIdx.y) * TY;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
   // Programmatic dependent launch (launch_2d): the next kernel of the stream
   // may start its CTAs now; this one waits for its predecessor before the
   // first access that can conflict with it (CH: reading the field the
@@ -150,7 +145,7 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
   asm volatile("griddepcontrol.launch_dependents;");
   if constexpr (M == Mode::CahnHilliard) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
-  load_tile_2d<TX, TY, PX, PY>(tile, bar, a, x0, y0);
+  load_tile_2d<TX, TY, PX, PY>(tile, a, x0, y0);
 
   const int tx = threadIdx.x % (TX / PX), ty = threadIdx.x / (TX / PX);
   const int lx = tx * PX + R;  // tile column of the first owned point
