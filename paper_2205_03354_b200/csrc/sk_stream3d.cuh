@@ -334,15 +334,15 @@ __device__ __forceinline__ void plane_slices(const double* base, const Args3D& a
 }
 
 #ifndef SK_A25_TY
-#define SK_A25_TY 16
-#define SK_A25_S 8
-#define SK_A25_MINB 2
+#define SK_A25_TY 8  // 64x8 tiles, 4 CTAs/SM (measured 59.5 us at 256^3; 64x16 x2: 60.7 us)
+#define SK_A25_S 6
+#define SK_A25_MINB 4
 #endif
 using Cfg3R2 = Cfg3<2, 64, SK_A25_TY, 2, 2, SK_A25_S, SK_A25_MINB>;    // 25-point apply
 #ifndef SK_CH3_TY  // experiments: -DSK_CH3_TY=.. -DSK_CH3_S=.. -DSK_CH3_MINB=..
-#define SK_CH3_TY 16
+#define SK_CH3_TY 8
 #define SK_CH3_S 8
-#define SK_CH3_MINB 1  // 1 CTA/SM: 194 registers, no spills (2 CTAs/SM spilled: 96 -> 82 us at 256^3)
+#define SK_CH3_MINB 2  // 64x8 tiles, 2 CTAs/SM, 198 registers, no spills (64x16 x2 spilled: 96 us; x1: 82 us; this: 71 us)
 #endif
 using Cfg3CH = Cfg3<2, 64, SK_CH3_TY, 2, 2, SK_CH3_S, SK_CH3_MINB>;    // 3D CH (7-point L f' + 25-point B)
 #ifndef SK_A73_TY
