@@ -154,3 +154,46 @@ def ch_temporal_convergence(dim: int, orders=(1, 2), n: int = 32, t_end: float =
             samples.append((dt, float(np.sqrt(np.sum((c - reference) ** 2)) / ref_norm)))
         fits.append(TemporalFit(order, fit_loglog(samples)))
     return fits
+
+
+@dataclass
+class BiharmonicResult:
+    """experiments.hpp BiharmonicResult"""
+    fit: ConvergenceFit = None
+    residuals: List[float] = field(default_factory=list)  # relative solver residual per ladder point
+
+
+def biharmonic_solve(interval_ladder: Sequence[int] = (8, 16, 32, 64), rel_tol: float = 1e-10,
+                     matrix_free: bool = False) -> BiharmonicResult:
+    """biharmonic_solve (experiments.cpp:99-143) on the device: the simply-supported
+    plate Delta^2 u = 4 pi^4 sin(pi x) sin(pi y) on the unit square, GPU assembly of
+    compose(laplacian(2, 2), itself), device CG (CSR, or the matrix-free operator),
+    max-norm error fit and relative residuals ||b - M x|| / ||b||."""
+    from .grid import BoundaryKind, DeviceStencil, GridSpec, assemble
+    from .kernels import csr_matvec
+    from .linalg import SolveOptions, cg_solve, cg_solve_stencil
+    from .stencil import compose, laplacian
+
+    lap = laplacian(2, 2)
+    bilap = DeviceStencil(compose(lap, lap))
+    result = BiharmonicResult()
+    samples = []
+    for intervals in interval_ladder:
+        h = 1.0 / intervals
+        g = GridSpec(dim=2, n=[intervals + 1] * 2, h=h, origin=[0.0, 0.0],
+                     bc=[BoundaryKind.simply_supported] * 2)
+        m = assemble(bilap, g)
+        nu = intervals - 1
+        coord = (np.arange(nu) + 1) * h  # GridSpec::coordinate (grid.cpp:37-40), simply supported
+        sxy = np.outer(np.sin(math.pi * coord), np.sin(math.pi * coord)).ravel()  # row = j * nu + i
+        b = 4.0 * math.pow(math.pi, 4) * sxy
+        opts = SolveOptions(rel_tol=rel_tol)
+        x = cg_solve_stencil(bilap, g, b, opts) if matrix_free else cg_solve(m, b, opts)
+        samples.append((h, float(np.max(np.abs(x - sxy)))))
+        xd = DeviceArray.from_host(x)
+        mx = DeviceArray(m.rows)
+        csr_matvec(m, xd, mx)
+        r = b - mx.to_host()
+        result.residuals.append(math.sqrt(float(np.dot(r, r)) / float(np.dot(b, b))))
+    result.fit = fit_loglog(samples)
+    return result

@@ -116,3 +116,22 @@ def test_temporal_convergence_orders():
     slopes = {f.order: f.fit.slope for f in fits}
     assert 0.8 <= slopes[1] <= 1.3, slopes
     assert 1.7 <= slopes[2] <= 2.5, slopes
+
+
+def test_biharmonic_solve_driver_vs_reference(ref):
+    # experiments.cpp:99-143 (the reference's own BVP driver): same fit and residual bar
+    import ctypes
+
+    from paper_2205_03354_b200.experiments import biharmonic_solve
+
+    ladder = [8, 16, 32, 64]
+    lad = np.ascontiguousarray(ladder, np.int32)
+    slope, coeff = ctypes.c_double(), ctypes.c_double()
+    res = np.empty(len(ladder))
+    assert ref.L.skref_biharmonic_solve(len(ladder), lad.ctypes.data, 1e-10, ctypes.byref(slope),
+                                        ctypes.byref(coeff), res.ctypes.data) == 0
+    for mf in (False, True):
+        r = biharmonic_solve(ladder, 1e-10, matrix_free=mf)
+        assert r.fit.slope == pytest.approx(slope.value, rel=1e-6)
+        assert r.fit.coefficient == pytest.approx(coeff.value, rel=1e-5)
+        assert max(r.residuals) <= 1e-10 and max(res) <= 1e-10
