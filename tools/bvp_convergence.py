@@ -36,6 +36,7 @@ from paper_2205_03354_b200 import _lib  # noqa: E402
 from paper_2205_03354_b200.device import DeviceArray  # noqa: E402
 from paper_2205_03354_b200.errors import StencilkitError  # noqa: E402
 from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, assemble, make_grid  # noqa: E402
+from paper_2205_03354_b200.experiments import fit_loglog  # noqa: E402
 from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve, cg_solve_stencil  # noqa: E402
 from paper_2205_03354_b200.stencil import bilaplacian  # noqa: E402
 
@@ -81,18 +82,6 @@ def refine(x_coarse: np.ndarray, dim: int, nc: int) -> np.ndarray:
     for ax in range(dim):
         v = refine_axis(v, ax)
     return v.ravel()
-
-
-def fit_loglog(samples):
-    """experiments.cpp:16-42."""
-    lx = np.log([h for h, _ in samples])
-    ly = np.log([e for _, e in samples])
-    n = len(samples)
-    sx, sy, sxx, sxy = lx.sum(), ly.sum(), (lx * lx).sum(), (lx * ly).sum()
-    slope = (n * sxy - sx * sy) / (n * sxx - sx * sx)
-    intercept = (sy - slope * sx) / n
-    resid = math.sqrt(((ly - (slope * lx + intercept)) ** 2).sum() / n)
-    return slope, math.exp(intercept), resid
 
 
 def main() -> None:
@@ -149,8 +138,8 @@ def main() -> None:
                           "nested_x0": use_x0, "status": status}), flush=True)
         del m, b, x
     if len(samples) >= 3:
-        slope, coeff, resid = fit_loglog(samples)
-        print(json.dumps({"fit": {"slope": slope, "coefficient": coeff, "fit_residual": resid},
+        fit = fit_loglog(samples)
+        print(json.dumps({"fit": {"slope": fit.slope, "coefficient": fit.coefficient, "fit_residual": fit.fit_residual},
                           "samples": samples}), flush=True)
 
 
