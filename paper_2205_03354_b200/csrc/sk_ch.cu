@@ -119,8 +119,8 @@ static bool chf3d_padded_ok(const GridInfo& g) {
 }
 
 static CUtensorMapL2promotion l2_promotion() {
-  const char* e = getenv("SK_TMA_L2");  // experiments: 0 / 64 / 128 / 256
-  const int v = e ? atoi(e) : 0;
+  const char* e = getenv("SK_TMA_L2");  // experiments: 0 (none) / 64 / 128 / 256
+  const int v = e ? atoi(e) : 64;  // 64 B promotion: measured +1.6% at 256^3, +10% at 1024^3
   return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
          : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
