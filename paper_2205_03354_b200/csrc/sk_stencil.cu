@@ -125,7 +125,12 @@ int check_width(const sk_stencil* s, const GridInfo& g) {
 }
 
 // ---- kernel configurations ----------------------------------------------
-using T2 = Tile2D<64, 32, 2, 4>;
+#ifndef SK_T2_TY  // experiments: 2D tile height, points per thread
+#define SK_T2_TY 32
+#define SK_T2_PX 2
+#define SK_T2_PY 4
+#endif
+using T2 = Tile2D<64, SK_T2_TY, SK_T2_PX, SK_T2_PY>;
 using C3R2 = Cfg3R2;
 using C3R4 = Cfg3R4;
 
@@ -141,10 +146,10 @@ int num_sms() {
 
 template <Mode M>
 int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
-  auto kern = stencil2d_kernel<M, 64, 32, 2, 4>;
+  auto kern = stencil2d_kernel<M, 64, SK_T2_TY, SK_T2_PX, SK_T2_PY>;
   static int once = set_smem(kern, T2::SMEM_BYTES);
   if (once != SK_OK) return once;
-  dim3 grid(unsigned((a.nx + 63) / 64), unsigned((a.ny + 31) / 32));
+  dim3 grid(unsigned((a.nx + 63) / 64), unsigned((a.ny + SK_T2_TY - 1) / SK_T2_TY));
   // programmatic dependent launch: overlaps this grid's ramp-up (tile loads
   // and, for Apply, the whole computation) with the predecessor's tail
   cudaLaunchConfig_t cfg{};
