@@ -181,6 +181,14 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
                    double* scratch_dev, int* result_is_scratch, void* stream);
 int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
                         const sk_ch_params* p, double dt, int64_t nsteps, double* c_host);
+/* One fused explicit step on a z-slab of a periodic 3D field (multi-GPU slab
+ * decomposition): g describes the slab (n[2] = its interior
+ * planes; x and y periodic); in_ghosted holds n[2] + 4 planes, two ghost
+ * planes below and above the interior (the neighbours' planes, exchanged by
+ * the caller); out receives the n[2] interior planes of c'. */
+int sk_ch_explicit_slab(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
+                        const sk_ch_params* p, double dt, const double* in_ghosted_dev, double* out_dev,
+                        void* stream);
 /* free_energy (cahn_hilliard.cpp:77-114): h^d sum f_chem + kappa/2 |central grad|^2 */
 int sk_free_energy(const sk_grid_desc* g, const sk_ch_params* p, const double* c_dev,
                    double* energy_host, void* stream);

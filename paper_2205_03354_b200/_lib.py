@@ -71,6 +71,7 @@ SIGNATURES = {
     "sk_composed_apply_host": (c_int, [vp, C.POINTER(GridDesc), vp, vp]),
     "sk_ch_explicit": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, c_i64, vp, vp,
                                C.POINTER(c_int), vp]),
+    "sk_ch_explicit_slab": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, vp, vp, vp]),
     "sk_ch_explicit_host": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, c_i64, vp]),
     "sk_free_energy": (c_int, [C.POINTER(GridDesc), C.POINTER(ChParams), vp, pd, vp]),
     "sk_ch_imex_create": (c_int, [C.POINTER(GridDesc), C.POINTER(ChParams), C.POINTER(SolveOptionsC),

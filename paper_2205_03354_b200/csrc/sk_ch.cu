@@ -183,7 +183,7 @@ static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
 // One fused step on the fast path (in -> out).
 static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
                         double dt, const double* in, double* out, cudaStream_t stream, bool bulk_ok_ptrs,
-                        int io = kIoPlain) {
+                        int io = kIoPlain, bool z_ghosted = false) {
   const double dtm = dt * p->mobility;
   const double fac_b = -dtm * p->kappa;
   const double sb = pow_int(g.h, bilap->h_power), sl = pow_int(g.h, lap->h_power);
@@ -220,6 +220,7 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   a.wl1 = wl1;
   a.chem = chem;
   a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R;
+  a.z_ghosted = z_ghosted ? 1 : 0;
   if (p->formulation == SK_CH_COMPOSED) return launch_3d<Mode::CahnHilliard, C3R2>(a, stream);
   // factored: mu = f' - kappa L c ; c' = c + dt M L mu
   a.kl0 = -p->kappa * (lap->orbit_coeff[0] * sl);
@@ -369,6 +370,25 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
       return st;
   }
   return SK_OK;
+}
+
+int sk_ch_explicit_slab(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* gd, const sk_ch_params* p,
+                        double dt, const double* in_ghosted, double* out, void* stream_p) {
+  if (!lap || !bilap || !p) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil or params");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (g.dim != 3) return fail(SK_ERR_INVALID_ARGUMENT, "slab stepping is 3D");
+  for (int a = 0; a < 3; ++a)
+    if (g.bc[a] != SK_BC_PERIODIC) return fail(SK_ERR_NON_PERIODIC, "Cahn-Hilliard runs on periodic grids");
+  if (!is_lap_shape(lap, 3) || !is_bilap_shape(bilap, 3))
+    return fail(SK_ERR_INVALID_ARGUMENT, "slab stepping needs the 7-point L and its 25-point composition");
+  if (g.n[0] < 5 || g.n[1] < 5) return fail(SK_ERR_STENCIL_WIDER_THAN_GRID, "periodic axis narrower than stencil support");
+  if (!(dt > 0)) return fail(SK_ERR_INVALID_ARGUMENT, "dt must be positive");
+  if (!in_ghosted || !out) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
+  const int64_t plane = g.n[0] * g.n[1];
+  const double* in = in_ghosted + 2 * plane;  // first interior plane
+  const bool ptr_ok = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  return ch_step_fast(lap, bilap, g, p, dt, in, out, as_stream(stream_p), ptr_ok, kIoPlain, /*z_ghosted=*/true);
 }
 
 int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* gd, const sk_ch_params* p,

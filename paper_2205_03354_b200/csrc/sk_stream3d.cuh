@@ -69,6 +69,7 @@ struct Args3D {
   Poly3 chem;        // CH: f'
   int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
   int bc[3];         // boundary kind per axis (nx, ny, nz are unknown counts); bulk path: periodic only
+  int z_ghosted;     // slab mode: planes -R..-1 and nz..nz+R-1 exist in memory around u (no z wrap)
   int zchunk;        // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
 };
 
@@ -205,7 +206,7 @@ struct PlaneLoader {
     } else {  // fallback: 8-byte copies, any boundary kind (odd nx, tiny, unaligned or non-periodic grids)
       double* buf = ring + stage * C::PLANE;
       double fz = 1.0;
-      const int64_t pz = bc_map(gze, a.nz, a.bc[2], fz);  // gze: the unwrapped plane index
+      const int64_t pz = a.z_ghosted ? gze : bc_map(gze, a.nz, a.bc[2], fz);  // gze: the unwrapped plane index
       const double* src = a.u + pz * a.nx * a.ny;
       for (int i = threadIdx.x; i < C::ROWS * C::WIDTH; i += C::THREADS) {
         const int r = i / C::WIDTH, c = i - r * C::WIDTH;
@@ -218,7 +219,7 @@ struct PlaneLoader {
           *d = f == 0.0 ? 0.0 : f * __ldg(src + gy * a.nx + gx);  // boundary zero / odd reflection
       }
     }
-    plane = gz + 1 == a.nz ? a.u : plane + a.nx * a.ny;
+    plane = (!a.z_ghosted && gz + 1 == a.nz) ? a.u : plane + a.nx * a.ny;
   }
 };
 
@@ -365,7 +366,7 @@ struct LoadCursor {
   __device__ __forceinline__ void start(const Args3D& a, const double* ring) {
     const Seg seg = seg_of<C>(a, u, uend);
     lze = seg.z0 - C::R;
-    lz = lze < 0 ? lze + int(a.nz) : lze;
+    lz = (lze < 0 && !a.z_ghosted) ? lze + int(a.nz) : lze;
     ld.setup(a, ring, seg.x0, seg.y0, lz);
     lp = 0;
     np = seg.len + 2 * C::R;
@@ -373,7 +374,7 @@ struct LoadCursor {
   __device__ __forceinline__ void issue_next(double* ring, int stage, const Args3D& a) {
     if (u < uend) {
       ld.issue(ring, stage, a, lz, lze);
-      lz = lz + 1 == a.nz ? 0 : lz + 1;
+      lz = (lz + 1 == a.nz && !a.z_ghosted) ? 0 : lz + 1;
       ++lze;
       if (++lp == np) {
         u += np - 2 * C::R;
