@@ -354,7 +354,12 @@ using Cfg3CH = Cfg3<2, 64, SK_CH3_TY, 2, 2, SK_CH3_S, SK_CH3_MINB>;    // 3D CH 
 #endif
 using Cfg3R4 = Cfg3<4, 64, SK_A73_TY, SK_A73_PX, 2, SK_A73_S, SK_A73_MINB>;    // 73-point apply
 using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
-using CfgChf3T = Cfg3<2, 64, 32, 2, 2, 8, 1>;  // factored 3D CH, TMA loads from ghost-padded fields
+#ifndef SK_CHT_TY
+#define SK_CHT_TY 32
+#define SK_CHT_S 8
+#define SK_CHT_MINB 1
+#endif
+using CfgChf3T = Cfg3<2, 64, SK_CHT_TY, 2, 2, SK_CHT_S, SK_CHT_MINB>;  // factored 3D CH, TMA loads from ghost-padded fields
 
 // Load cursor: walks the block's segment/plane sequence S-1 planes ahead of
 // the compute loop. The per-segment setup (64-bit divisions, wrapped source
