@@ -349,10 +349,11 @@ using Cfg3CH = Cfg3<2, 64, SK_CH3_TY, 2, 2, SK_CH3_S, SK_CH3_MINB>;    // 3D CH 
 #ifndef SK_A73_TY
 #define SK_A73_TY 16
 #define SK_A73_PX 2
+#define SK_A73_PY 2
 #define SK_A73_S 8
 #define SK_A73_MINB 1
 #endif
-using Cfg3R4 = Cfg3<4, 64, SK_A73_TY, SK_A73_PX, 2, SK_A73_S, SK_A73_MINB>;    // 73-point apply
+using Cfg3R4 = Cfg3<4, 64, SK_A73_TY, SK_A73_PX, SK_A73_PY, SK_A73_S, SK_A73_MINB>;    // 73-point apply
 using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
 #ifndef SK_CHT_TY
 #define SK_CHT_TY 32
