@@ -11,17 +11,23 @@
 //       raises CHECK when sqrt(rho) <= tol ||b|| (linalg.cpp:31) or stops at
 //       max_iter.
 //   K3  p = r + beta p (bit-exact xpby).
+// Matrix-free operators replace K1 by the stencil apply + a p.q pass; on a
+// 2D 13-point class stencil the iteration is two kernels instead (fused2d):
+// the apply forms p' = r + beta p while loading its tile, writes q = A p' and
+// reduces alpha; K2 recomputes p' (same bits), stores it and updates x, r.
 // Kernels of a graph become no-ops once the status leaves RUNNING, so the
 // iteration count is exact. The rare true-residual check / restart
 // (linalg.cpp:32-47) and the final acceptance test (:59-66) run outside the
 // graph.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <string>
 
 #include "sk_internal.hpp"
+#include "sk_cgstate.cuh"
 #include "sk_sell.cuh"
 
 namespace sk {
@@ -29,17 +35,8 @@ namespace sk {
 namespace {
 
 constexpr int kT = 256;
-enum : int { kRunning = 0, kCheck = 1, kNotPD = 2, kMaxIter = 3 };
-constexpr int kLoopUnroll = 4;  // CG iterations per round of the device-side while loop
-
-struct CgState {
-  double rho, pq, alpha, beta, target;
-  double scalar_out;  // result slot of auxiliary reductions
-  int64_t it, max_iter;
-  int status;
-  int pad;
-  unsigned counter[4];
-};
+enum : int { kRunning = kCgRunning, kCheck = kCgCheck, kNotPD = kCgNotPD, kMaxIter = kCgMaxIter };
+constexpr int kLoopUnroll = 4;  // CG iterations per round of the device-side while loop (even: see fused2d)
 
 // Row i of M times x from the SELL-32 copy (sk_sell.cuh): reference order and rounding.
 template <class IDX>
@@ -66,23 +63,36 @@ __global__ void __launch_bounds__(kT) k1_spmv_pq(int64_t n, const int64_t* __res
   if (threadIdx.x == 0) partials[blockIdx.x] = acc;
   if (last_block(&st->counter[0])) {
     const double pq = reduce_partials<kT>(partials, gridDim.x, sh);
-    if (threadIdx.x == 0) {
-      st->pq = pq;
-      if (pq <= 0) st->status = kNotPD;
-      else st->alpha = st->rho / pq;
-    }
+    if (threadIdx.x == 0) cg_publish_pq(st, pq);
   }
 }
 
-__global__ void __launch_bounds__(kT) k2_update_rr(int64_t n, const double* __restrict__ p, const double* __restrict__ q,
+// FUSED (2D fused path, which has no K3): K3 of the previous iteration is
+// deferred to here, p' = r + beta p (the same bits the apply formed) stored
+// before the updates use it, and the last CTA publishes the device-side while
+// loop's condition (COND). The new beta is written after every CTA has read
+// the old one (last_block orders it).
+template <bool COND, bool FUSED>
+__global__ void __launch_bounds__(kT) k2_update_rr(int64_t n, double* __restrict__ p, const double* __restrict__ q,
                                                    double* __restrict__ x, double* __restrict__ r, CgState* st,
-                                                   double* partials) {
-  if (st->status != kRunning) return;
+                                                   double* partials, cudaGraphConditionalHandle cond) {
+  if (st->status != kRunning) {
+    if constexpr (COND) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+    }
+    return;
+  }
   __shared__ double sh[32];
   const double alpha = st->alpha, nalpha = -alpha;
+  const double beta = FUSED ? st->beta : 0.0;
   double acc = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
-    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));            // axpy(alpha, p, x)
+    double pi = p[i];
+    if constexpr (FUSED) {
+      pi = __dadd_rn(r[i], __dmul_rn(beta, pi));  // xpby(r, beta, p)
+      p[i] = pi;
+    }
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));               // axpy(alpha, p, x)
     const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, q[i]));  // axpy(-alpha, q, r)
     r[i] = ri;
     acc = fma(ri, ri, acc);
@@ -97,6 +107,7 @@ __global__ void __launch_bounds__(kT) k2_update_rr(int64_t n, const double* __re
       st->it += 1;
       if (st->it >= st->max_iter) st->status = kMaxIter;
       else if (sqrt(rho_next) <= st->target) st->status = kCheck;
+      if constexpr (COND) cudaGraphSetConditional(cond, st->status == kRunning ? 1u : 0u);
     }
   }
 }
@@ -139,6 +150,7 @@ __global__ void __launch_bounds__(kT) k_true_residual(int64_t n, const int64_t* 
 }
 
 // restart: r = b - q ; p = r ; rho = r.r   (linalg.cpp:43-46)
+// (beta = 0: the fused path's deferred p' = r + 0 p is then r)
 __global__ void __launch_bounds__(kT) k_restart(int64_t n, const double* __restrict__ b, const double* __restrict__ q,
                                                 double* __restrict__ r, double* __restrict__ p, CgState* st,
                                                 double* partials) {
@@ -156,6 +168,7 @@ __global__ void __launch_bounds__(kT) k_restart(int64_t n, const double* __restr
     const double t = reduce_partials<kT>(partials, gridDim.x, sh);
     if (threadIdx.x == 0) {
       st->rho = t;
+      st->beta = 0.0;
       st->status = kRunning;
     }
   }
@@ -193,11 +206,7 @@ __global__ void __launch_bounds__(kT) k_pq(int64_t n, const double* __restrict__
   if (threadIdx.x == 0) partials[blockIdx.x] = acc;
   if (last_block(&st->counter[0])) {
     const double pq = reduce_partials<kT>(partials, gridDim.x, sh);
-    if (threadIdx.x == 0) {
-      st->pq = pq;
-      if (pq <= 0) st->status = kNotPD;
-      else st->alpha = st->rho / pq;
-    }
+    if (threadIdx.x == 0) cg_publish_pq(st, pq);
   }
 }
 
@@ -232,10 +241,13 @@ struct CgPlan {
   CgState* st = nullptr;  // device
   double* partials = nullptr;
   double *r = nullptr, *p = nullptr, *q = nullptr;
+  // fused2d: 2D class-1 stencil operator; each iteration is two kernels,
+  // [q = A (r + beta p) ; alpha] and [p = r + beta p ; x, r update ; beta]
+  bool fused2d = false;
   cudaGraphExec_t exec = nullptr;
   const double* graph_x = nullptr;
   bool device_loop = false;  // exec = while(status == running) { iteration } on the device
-  int kernels_per_iteration() const { return op.m ? 3 : 4; }
+  int kernels_per_iteration() const { return fused2d ? 2 : (op.m ? 3 : 4); }
 
   ~CgPlan() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -329,8 +341,17 @@ struct CgPlan {
     return SK_OK;
   }
   int iteration(double* x, cudaStream_t cap, bool cond, cudaGraphConditionalHandle h) {
+    if (fused2d) {
+      if (int e = launch_cg_apply_2d(op.s, op.g, p, r, q, st, partials, cap)) return e;
+      if (cond)
+        k2_update_rr<true, true><<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials, h);
+      else
+        k2_update_rr<false, true><<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials, h);
+      SK_LAUNCH_CHECK("k2_update_rr");
+      return SK_OK;
+    }
     if (int e = launch_q(cap)) return e;
-    k2_update_rr<<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials);
+    k2_update_rr<false, false><<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials, h);
     if (cond)
       k3_xpby<true><<<grid, kT, 0, cap>>>(n, r, p, st, h);
     else
@@ -381,6 +402,15 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
   pl->check_every = check_every > 0 ? check_every : 64;
   const int64_t g = (op.n + kT - 1) / kT;
   pl->grid = int(g > int64_t(kNumSMs) * 8 ? int64_t(kNumSMs) * 8 : (g > 0 ? g : 1));
+  int partials = pl->grid;
+  if (op.s) {
+    const char* env = getenv("SK_CG_FUSED");
+    const int ctas = cg_apply_2d_ctas(op.s, op.g);
+    if (ctas > 0 && !(env && env[0] == '0')) {
+      pl->fused2d = true;
+      partials = std::max(partials, ctas);
+    }
+  }
   if (op.m) {
     if (int e = csr_build_sell(const_cast<sk_csr*>(op.m), stream)) {  // before any graph capture
       delete pl;
@@ -388,7 +418,7 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
     }
   }
   const size_t vec = sizeof(double) * size_t(op.n > 0 ? op.n : 1);
-  const size_t ws_bytes = 3 * vec + sizeof(double) * size_t(pl->grid) + sizeof(CgState) + 256;
+  const size_t ws_bytes = 3 * vec + sizeof(double) * size_t(partials) + sizeof(CgState) + 256;
   if (cudaMalloc(reinterpret_cast<void**>(&pl->ws), ws_bytes) != cudaSuccess) {
     delete pl;
     return fail(SK_ERR_OUT_OF_MEMORY, "cg workspace");
@@ -397,7 +427,7 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
   pl->p = pl->r + op.n;
   pl->q = pl->p + op.n;
   pl->partials = pl->q + op.n;
-  pl->st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(pl->partials + pl->grid) + 127) & ~uintptr_t(127));
+  pl->st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(pl->partials + partials) + 127) & ~uintptr_t(127));
   *out = pl;
   return SK_OK;
 }

@@ -158,19 +158,20 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // "Last block done" ticket: returns true in every thread of the CTA that
 // finishes last; that CTA then combines the per-CTA partials in index order,
 // so the two-level reduction is deterministic for a given grid size.
-__device__ __forceinline__ bool last_block(unsigned* counter) {
+__device__ __forceinline__ bool last_block(unsigned* counter, unsigned nblocks) {
   __shared__ bool is_last;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned ticket = atomicAdd(counter, 1u);
-    is_last = ticket == gridDim.x - 1;
+    is_last = ticket == nblocks - 1;
     if (is_last) *counter = 0;  // reset for the next launch
   }
   __syncthreads();
   if (is_last) __threadfence();
   return is_last;
 }
+__device__ __forceinline__ bool last_block(unsigned* counter) { return last_block(counter, gridDim.x); }
 
 // Sum the per-CTA partials in a fixed order (called by the last CTA only).
 template <int THREADS>

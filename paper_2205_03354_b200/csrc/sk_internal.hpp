@@ -63,7 +63,19 @@ int csr_build_sell(sk_csr* m, cudaStream_t stream);
 int check_width(const sk_stencil* s, const GridInfo& g);
 
 // Launch one matrix-free application on `stream` (device pointers).
-int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream);
+// input_stable: u is not written by the kernel launched just before, so the
+// 2D kernel may load it before its programmatic-launch wait.
+int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream,
+                 bool input_stable = false);
+
+// Fused matrix-free CG half-iteration on a 2D class-1 stencil (Mode::CgApply):
+// q = A p' with p' = r + beta p formed on the load, alpha from p'.q.
+// cg_apply_2d_ctas: CTA count (the partials it needs), 0 when the
+// stencil/grid is not eligible.
+struct CgState;
+int cg_apply_2d_ctas(const sk_stencil* s, const GridInfo& g);
+int launch_cg_apply_2d(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
+                       CgState* st, double* partials, cudaStream_t stream);
 
 // ---- conjugate gradients (sk_cg.cu) ----
 // The operator q = A p: an assembled CSR (SELL SpMV, bit-identical to the

@@ -147,7 +147,8 @@ int num_sms() {
 template <Mode M>
 int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
   auto kern = stencil2d_kernel<M, 64, SK_T2_TY, SK_T2_PX, SK_T2_PY>;
-  static int once = set_smem(kern, T2::SMEM_BYTES);
+  constexpr int smem = M == Mode::CgApply ? T2::SMEM_BYTES_CG : T2::SMEM_BYTES;
+  static int once = set_smem(kern, smem);
   if (once != SK_OK) return once;
   dim3 grid(unsigned((a.nx + 63) / 64), unsigned((a.ny + SK_T2_TY - 1) / SK_T2_TY));
   // programmatic dependent launch: overlaps this grid's ramp-up (tile loads
@@ -155,7 +156,7 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(T2::THREADS);
-  cfg.dynamicSmemBytes = T2::SMEM_BYTES;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -163,7 +164,9 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const char* env = getenv("SK_PDL");
-  if (env && env[0] == '0') cfg.numAttrs = 0;
+  // (the fused CG apply follows K2 of the previous iteration: measured slower
+  // with the programmatic edge)
+  if ((env && env[0] == '0') || M == Mode::CgApply) cfg.numAttrs = 0;
   SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
   SK_LAUNCH_CHECK("stencil2d_kernel");
   return SK_OK;
@@ -184,6 +187,31 @@ int launch_3d(Args3D a, cudaStream_t stream) {
 }
 
 template int launch_2d<Mode::CahnHilliard>(const Apply2DArgs&, cudaStream_t);
+
+int cg_apply_2d_ctas(const sk_stencil* s, const GridInfo& g) {
+  if (s->kclass != 1 || g.dim != 2) return 0;
+  for (int a = 0; a < 2; ++a)
+    if (g.un[a] < 5) return 0;  // streamable at radius 2
+  return int(((g.un[0] + 63) / 64) * ((g.un[1] + SK_T2_TY - 1) / SK_T2_TY));
+}
+
+int launch_cg_apply_2d(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
+                       CgState* st, double* partials, cudaStream_t stream) {
+  if (!cg_apply_2d_ctas(s, g)) return fail(SK_ERR_INVALID_ARGUMENT, "fused CG apply needs a 2D class-1 stencil");
+  const double scale = pow_int(g.h, s->h_power);
+  Apply2DArgs a{};
+  for (int i = 0; i < 8; ++i) a.w.w[i] = s->orbit_coeff[i] * scale;
+  a.u = p;
+  a.v = q;
+  a.nx = g.un[0];
+  a.ny = g.un[1];
+  a.bc[0] = g.bc[0];
+  a.bc[1] = g.bc[1];
+  a.r = r;
+  a.st = st;
+  a.partials = partials;
+  return launch_2d<Mode::CgApply>(a, stream);
+}
 template int launch_3d<Mode::CahnHilliard, Cfg3CH>(Args3D, cudaStream_t);
 
 int launch_generic(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream) {
@@ -225,7 +253,8 @@ static bool streamable(const sk_stencil* s, const GridInfo& g, int radius) {
   return true;
 }
 
-int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream) {
+int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream,
+                 bool input_stable) {
   const double scale = pow_int(g.h, s->h_power);
   OrbitW w{};
   for (int i = 0; i < 8; ++i) w.w[i] = s->orbit_coeff[i] * scale;  // == coeff.to_double()*pow_int (grid.cpp:80)
@@ -239,6 +268,7 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     a.w = w;
     a.bc[0] = g.bc[0];
     a.bc[1] = g.bc[1];
+    a.input_stable = input_stable;
     a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= 64 + 4 && a.ny >= 32 + 4 && aligned16(u) && aligned16(v);
     return launch_2d<Mode::Apply>(a, stream);
   }
@@ -358,7 +388,7 @@ int sk_composed_apply_repeat(const sk_stencil* s_c, const sk_grid_desc* gd, cons
     cudaStream_t cap = stream ? stream : capture_stream();
     SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     int st = SK_OK;
-    for (int r = 0; r < repeats && st == SK_OK; ++r) st = launch_apply(s, g, u, (r % 2) ? v1 : v0, cap);
+    for (int r = 0; r < repeats && st == SK_OK; ++r) st = launch_apply(s, g, u, (r % 2) ? v1 : v0, cap, /*input_stable=*/true);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap, &graph);
     if (st != SK_OK) {

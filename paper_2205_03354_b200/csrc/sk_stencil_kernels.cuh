@@ -28,6 +28,7 @@
 
 #include <cstdint>
 
+#include "sk_cgstate.cuh"
 #include "sk_common.cuh"
 
 namespace sk {
@@ -63,7 +64,12 @@ __device__ __forceinline__ double poly3(double c, const Poly3& p) {
   return fma(fma(fma(p.k3, c, p.k2), c, p.k1), c, p.k0);
 }
 
-enum class Mode { Apply = 0, CahnHilliard = 1 };
+// CgApply: one matrix-free CG iteration's first half (sk_cg.cu, fused2d):
+// p' = r + beta p formed on the tile load (the bit-exact xpby of
+// linalg.cpp:57, deferred from the previous iteration), q = A p', and the
+// p'.q partials reduced to alpha by the last CTA. p itself is not written:
+// the update kernel that follows recomputes p' and stores it.
+enum class Mode { Apply = 0, CahnHilliard = 1, CgApply = 2 };
 
 // Apply outputs are never re-read by the next launch (config 1 ping-pongs
 // outputs from a fixed input): stream them past L2 (evict-first) so the input
@@ -89,6 +95,7 @@ struct Tile2D {
   static constexpr int ROWS = TY + 2 * R;
   static constexpr int THREADS = (TX / PX) * (TY / PY);
   static constexpr int SMEM_BYTES = ROWS * PITCH * 8 + 16;
+  static constexpr int SMEM_BYTES_CG = 2 * ROWS * PITCH * 8 + 16;  // + the r tile
 };
 
 struct Apply2DArgs {
@@ -100,20 +107,59 @@ struct Apply2DArgs {
   Poly3 chem;
   int bulk_ok;   // 1: nx even and >= TX+4, periodic -> 16-byte cp.async rows
   int bc[2];     // boundary kind per axis (nx, ny are unknown counts)
+  int input_stable;  // Apply: u is not written by the preceding kernel (early loads under PDL)
+  // CgApply: u = p (previous direction), v = q
+  const double* __restrict__ r;
+  CgState* st;
+  double* partials;  // one per CTA
 };
 
-template <int TX, int TY, int PX, int PY>
+template <Mode M, int TX, int TY, int PX, int PY>
 __device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a, int64_t x0, int64_t y0) {
   using T = Tile2D<TX, TY, PX, PY>;
   constexpr int R = T::R;
   const int tid = threadIdx.x;
-  if (a.bulk_ok) {
+  // tile wholly inside the grid: no boundary map
+  const bool inner = x0 >= R && x0 + TX + R <= a.nx && y0 >= R && y0 + TY + R <= a.ny;
+  if constexpr (M == Mode::CgApply) {
+    const double beta = a.st->beta;
+    if (inner) {  // both tiles by 8-byte cp.async, then p' in place (each thread its own points)
+      double* rt = tile + T::ROWS * T::PITCH;
+      const int64_t base = (y0 - R) * a.nx + (x0 - R);
+      for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {
+        const int r = i / T::PITCH, c = i - r * T::PITCH;
+        const int64_t g = base + r * a.nx + c;
+        cp_async8(tile + i, a.u + g);
+        cp_async8(rt + i, a.r + g);
+      }
+      cp_async_wait_all();
+      for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) tile[i] = __dadd_rn(rt[i], __dmul_rn(beta, tile[i]));
+      __syncthreads();
+      return;
+    }
+    for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {
+      const int r = i / T::PITCH, c = i % T::PITCH;
+      double f = 1.0;
+      const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
+      const int64_t g = gy * a.nx + gx;
+      tile[i] = f == 0.0 ? 0.0 : f * __dadd_rn(__ldg(a.r + g), __dmul_rn(beta, __ldg(a.u + g)));
+    }
+    __syncthreads();
+  } else if (a.bulk_ok) {
     // every thread issues 16-byte cp.async (LDGSTS) pairs of the haloed tile
     constexpr int HP = T::PITCH / 2;
     for (int i = tid; i < T::ROWS * HP; i += T::THREADS) {
       const int r = i / HP, c = 2 * (i - r * HP);
       const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
       cp_async16(tile + r * T::PITCH + c, a.u + gy * a.nx + gx);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  } else if (inner) {  // 8-byte cp.async (rows need not be 16-byte aligned)
+    const int64_t base = (y0 - R) * a.nx + (x0 - R);
+    for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {
+      const int r = i / T::PITCH, c = i - r * T::PITCH;
+      cp_async8(tile + i, a.u + base + r * a.nx + c);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -139,13 +185,17 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
   const int64_t x0 = int64_t(blockIdx.x) * TX, y0 = int64_t(blockIdx.y) * TY;
   // Programmatic dependent launch (launch_2d): the next kernel of the stream
   // may start its CTAs now; this one waits for its predecessor before the
-  // first access that can conflict with it (CH: reading the field the
-  // predecessor wrote; Apply: overwriting the buffer the one before wrote).
+  // first access that can conflict with it: the first load, except for an
+  // Apply whose input no predecessor writes (the repeated apply of config 1),
+  // which loads and computes first and waits before overwriting its output.
   // Without the launch attribute both instructions are no-ops.
   asm volatile("griddepcontrol.launch_dependents;");
-  if constexpr (M == Mode::CahnHilliard) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (M != Mode::Apply || !a.input_stable) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if constexpr (M == Mode::CgApply) {
+    if (a.st->status != kCgRunning) return;  // uniform: set by the previous iteration
+  }
   __syncthreads();
-  load_tile_2d<TX, TY, PX, PY>(tile, a, x0, y0);
+  load_tile_2d<M, TX, TY, PX, PY>(tile, a, x0, y0);
 
   const int tx = threadIdx.x % (TX / PX), ty = threadIdx.x / (TX / PX);
   const int lx = tx * PX + R;  // tile column of the first owned point
@@ -208,6 +258,7 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
 
   const int64_t gx = x0 + tx * PX;
   if constexpr (M == Mode::Apply) asm volatile("griddepcontrol.wait;" ::: "memory");
+  double pq = 0.0;
 #pragma unroll
   for (int j = 0; j < PY; ++j) {
     const int64_t gy = y0 + ly + j;
@@ -219,13 +270,32 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
       val[i] = acc[j][i];
       if (M == Mode::CahnHilliard) val[i] += tile[(ly + j + R) * T::PITCH + lx + i];
     }
-    if (a.bulk_ok && PX % 2 == 0 && gx + PX <= a.nx) {
+    if constexpr (M == Mode::CgApply) {
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        if (gx + i < a.nx) {
+          const double p = tile[(ly + j + R) * T::PITCH + lx + i];
+          out[i] = val[i];
+          pq = fma(p, val[i], pq);
+        }
+      }
+    } else if (a.bulk_ok && PX % 2 == 0 && gx + PX <= a.nx) {
 #pragma unroll
       for (int i = 0; i < PX; i += 2) store_f64x2<M>(out + i, val[i], val[i + 1]);
     } else {
 #pragma unroll
       for (int i = 0; i < PX; ++i)
         if (gx + i < a.nx) out[i] = val[i];
+    }
+  }
+  if constexpr (M == Mode::CgApply) {
+    __shared__ double red[32];
+    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x, nctas = gridDim.x * gridDim.y;
+    pq = block_sum<T::THREADS>(pq, red);
+    if (threadIdx.x == 0) a.partials[cta] = pq;
+    if (last_block(&a.st->counter[0], nctas)) {
+      pq = reduce_partials<T::THREADS>(a.partials, int(nctas), red);
+      if (threadIdx.x == 0) cg_publish_pq(a.st, pq);
     }
   }
 }

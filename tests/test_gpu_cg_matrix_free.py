@@ -51,3 +51,30 @@ def test_matrix_free_and_csr_cg_agree_config2():
     x1 = cg_solve(m, b, o)
     x2 = cg_solve_stencil(s, g, b, o)
     assert np.linalg.norm(x1 - x2) <= 1e-6 * np.linalg.norm(x1)
+
+
+@pytest.mark.parametrize("bc", [BoundaryKind.clamped, BoundaryKind.simply_supported, BoundaryKind.periodic])
+@pytest.mark.parametrize("check_every", [0, 7])
+def test_fused_2d_iteration_matches_unfused(monkeypatch, bc, check_every):
+    # the two-kernel 2D iteration (p' = r + beta p on the tile load, p.q in
+    # the apply's epilogue) follows the four-kernel one: same recurrence, only
+    # the p.q summation order differs. Odd check_every exercises the p / p2
+    # parity of the unrolled graph (rounded up to even); the periodic Laplacian
+    # class is singular, so that case solves a mean-free right-hand side.
+    N = 96
+    g = make_grid(2, N + 1, 1.0 / N, bc)
+    b = np.sin(np.arange(g.unknown_count()) * 0.013) + (0.0 if bc == BoundaryKind.periodic else 1.0)
+    b -= b.mean() if bc == BoundaryKind.periodic else 0.0
+    o = SolveOptions(rel_tol=1e-9, check_every=check_every, deflate_mean=bc == BoundaryKind.periodic)
+    if check_every:
+        monkeypatch.setenv("SK_CG_DEVICE_LOOP", "0")  # the unrolled-graph fallback
+    reps = []
+    xs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("SK_CG_FUSED", fused)
+        rep = SolveReport()
+        xs.append(cg_solve_stencil(DeviceStencil(bilaplacian(2)), g, b, o, rep))  # new stencil -> new plan
+        reps.append(rep)
+    assert abs(reps[0].iterations - reps[1].iterations) <= 2
+    assert reps[0].true_rel_residual <= 1e-9
+    assert np.linalg.norm(xs[0] - xs[1]) <= 1e-7 * np.linalg.norm(xs[1])
