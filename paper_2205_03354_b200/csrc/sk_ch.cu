@@ -155,15 +155,12 @@ static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo&
   return SK_OK;
 }
 
-template <class C, int V, int LD, int OUT>
-static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
-  using SM = ChfSmem<C, LD>;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(chf3d_kernel<C, V, LD, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+template <class C, int V, int LD, int OUT, bool FB>
+static int launch_chf3d_as(const Args3D& a, const CUtensorMap& tm, int64_t grid, cudaStream_t stream) {
+  using SM = ChfSmem<C, LD, FB>;
+  auto kern = chf3d_kernel<C, V, LD, OUT, FB>;
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
   if (attr != cudaSuccess) return cuda_fail(attr, "chf3d smem attribute");
-  // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
-  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
-  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(C::THREADS);
@@ -175,9 +172,22 @@ static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
   cfg.attrs = at;
   const char* env = getenv("SK_PDL");
   cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
-  SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, chf3d_kernel<C, V, LD, OUT>, a, tm));
+  SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, tm));
   SK_LAUNCH_CHECK("chf3d_kernel");
   return SK_OK;
+}
+
+template <class C, int V, int LD, int OUT>
+static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
+  // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
+  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
+  // cp.async loads: the 16-byte or the 8-byte fallback instantiation (after
+  // persistent_grid, which may clear bulk_ok); TMA loads need neither
+  if constexpr (LD == 0) {
+    if (!a.bulk_ok) return launch_chf3d_as<C, V, LD, OUT, true>(a, tm, grid, stream);
+  }
+  return launch_chf3d_as<C, V, LD, OUT, false>(a, tm, grid, stream);
 }
 
 // One fused step on the fast path (in -> out).

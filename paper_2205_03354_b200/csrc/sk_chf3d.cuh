@@ -61,7 +61,7 @@ constexpr int kTmaSplit = SK_TMA_SPLIT;  // TMA boxes per plane
 // 128 B-aligned pitch C::PITCH). LD 1: one TMA box per plane from a
 // ghost-padded field (kPadL / kPadT below, see OUT 1) into dense stages of
 // pitch C::WIDTH; no wrap logic, no per-thread copy instructions.
-template <class C, int LD = 0>
+template <class C, int LD = 0, bool FB = false>
 struct ChfSmem {
   // LD 1 boxes start XO = 4 columns left of the tile and are 72 wide: whole
   // 32 B sectors from the 128 B-aligned padded rows, and a 576 B pitch whose
@@ -74,7 +74,9 @@ struct ChfSmem {
   static constexpr int MP = C::TX + 4;              // mu ring pitch: x in [-1, TX] at column x + 2
   static constexpr int MU_ROWS = C::TY + 2;         // y in [-1, TY]
   static constexpr int MU_PLANE = MU_ROWS * MP;
-  static constexpr int BYTES = RING_OFS + (C::STAGES * PLANE + 3 * MU_PLANE) * 8;
+  // LD 0 with the 8-byte fallback loader (FB): its boundary-map table after the mu ring
+  static constexpr int TAB = C::STAGES * PLANE + 3 * MU_PLANE;  // doubles from the ring
+  static constexpr int BYTES = RING_OFS + TAB * 8 + (FB ? C::TABLE_BYTES : 0);
   static constexpr int WARPS = C::THREADS / 32;
   static constexpr int BORDER_ROWS = 2 * (C::TX + 2);                     // mu rows -1 and TY, x in [-1, TX]
   static constexpr int ROWS_PER_WARP = (BORDER_ROWS + WARPS - 1) / WARPS;  // + 4 side points per warp
@@ -120,12 +122,12 @@ struct TmaCursor {
 // a ghost-padded field at a.v and its periodic images into the 2-wide ghost
 // frame (the next step's TMA boxes then never wrap). LD 1 / OUT 1 need whole
 // tiles (nx % TX == 0, ny % TY == 0).
-template <class C, int V = 0, int LD = 0, int OUT = 0>
+template <class C, int V = 0, int LD = 0, int OUT = 0, bool FB = false>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
     chf3d_kernel(const __grid_constant__ Args3D a, const __grid_constant__ CUtensorMap tmap) {
   constexpr int R = 2, S = C::STAGES;
   static_assert(C::R == 2 && C::PX == 2 && C::PY == 2 && C::TX == 64, "factored CH kernel layout: warp = row pair");
-  using SM = ChfSmem<C, LD>;
+  using SM = ChfSmem<C, LD, FB>;
   constexpr int P = SM::P, PLANE = SM::PLANE, MP = SM::MP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw + SM::RING_OFS);
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   const int per = units / G, rem = units % G;
   const int ubeg = b * per + (b < rem ? b : rem);
   const int uend = ubeg + per + (b < rem ? 1 : 0);
-  LoadCursor<C> lc;
+  LoadCursor<C, FB, SM::TAB> lc;
   TmaCursor<C> tc;
   int s_load = 0;
   // programmatic dependent launch: wait for the previous step (which wrote

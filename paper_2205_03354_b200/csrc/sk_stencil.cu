@@ -174,14 +174,19 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
 
 template <Mode M, class C>
 int launch_3d(Args3D a, cudaStream_t stream) {
-  auto kern = stream3d_kernel<M, C>;
-  static int once = set_smem(kern, C::SMEM_BYTES);
+  auto bulk = stream3d_kernel<M, C, false>;
+  auto fallback = stream3d_kernel<M, C, true>;
+  constexpr int bulk_smem = C::SMEM_BYTES - C::TABLE_BYTES;  // no boundary-map table
+  static int once = set_smem(bulk, bulk_smem) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, C::SMEM_BYTES);
   if (once != SK_OK) return once;
   // lockstep for the radius-2 apply (halo rows from L2), balanced for the
   // issue-bound radius-4 apply and the composed CH step (measured at 256^3)
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/C::R == 2 && M == Mode::Apply);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
-  kern<<<unsigned(grid), C::THREADS, C::SMEM_BYTES, stream>>>(a);
+  if (a.bulk_ok)  // (after persistent_grid, which may clear it)
+    bulk<<<unsigned(grid), C::THREADS, bulk_smem, stream>>>(a);
+  else
+    fallback<<<unsigned(grid), C::THREADS, C::SMEM_BYTES, stream>>>(a);
   SK_LAUNCH_CHECK("stream3d_kernel");
   return SK_OK;
 }
@@ -388,7 +393,8 @@ int sk_composed_apply_repeat(const sk_stencil* s_c, const sk_grid_desc* gd, cons
     cudaStream_t cap = stream ? stream : capture_stream();
     SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     int st = SK_OK;
-    for (int r = 0; r < repeats && st == SK_OK; ++r) st = launch_apply(s, g, u, (r % 2) ? v1 : v0, cap, /*input_stable=*/true);
+    for (int r = 0; r < repeats && st == SK_OK; ++r)
+      st = launch_apply(s, g, u, (r % 2) ? v1 : v0, cap, /*input_stable=*/true);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap, &graph);
     if (st != SK_OK) {

@@ -54,7 +54,8 @@ struct Cfg3 {
   static_assert(CONSUMERS % 32 == 0, "consumer threads must be whole warps");
   static_assert(PX % 2 == 0 && R % 2 == 0, "128-bit row loads need even PX and R");
   static constexpr int THREADS = CONSUMERS;
-  static constexpr int SMEM_BYTES = RING_OFS + STAGES * PLANE * 8;
+  static constexpr int TABLE_BYTES = ROWS * WIDTH * 8;  // boundary map of the 8-byte fallback loader
+  static constexpr int SMEM_BYTES = RING_OFS + STAGES * PLANE * 8 + TABLE_BYTES;
   static constexpr int Q = 2 * R + 1;
 };
 
@@ -160,7 +161,11 @@ __host__ __device__ constexpr int num_kinds() { return R >= 4 ? 8 : 4; }
 // every plane of a segment: the wrapped source pointers are computed once per
 // segment and advanced by one plane per issue, the shared-memory addresses
 // are precomputed, so a 16-byte pair costs an add, a 64-bit add and an LDGSTS.
-template <class C>
+// FB: the 8-byte fallback loader (kernels are instantiated for both and
+// launched with FB = !bulk_ok, so the 16-byte path carries no fallback code).
+// TAB: offset of the fallback's boundary-map table from the ring (doubles;
+// the stream kernels keep it right after the ring).
+template <class C, bool FB, int TAB = C::STAGES * C::PLANE>
 struct PlaneLoader {
   static constexpr int HP = C::WIDTH / 2;  // 16-byte chunks per row
   static constexpr int NP = (C::ROWS * HP + C::THREADS - 1) / C::THREADS;
@@ -172,22 +177,43 @@ struct PlaneLoader {
   __device__ __forceinline__ static bool used(int k) {
     return k + 1 < NP || int(threadIdx.x) + k * C::THREADS < C::ROWS * HP;
   }
+  // 8-byte fallback: the tile's boundary map (it depends on x0, y0 only) is
+  // tabulated once per segment at ring + TAB: entry i = (source, shared
+  // offset), source = in-plane offset o >= 0 (copy), -1 (boundary zero) or
+  // -2 - o (odd reflection: negated copy). Each thread writes and reads only
+  // its own entries (i = tid mod THREADS): no barrier.
+  static constexpr int NT = C::ROWS * C::WIDTH;
+  __device__ __forceinline__ static int2* table(const double* ring) {
+    return reinterpret_cast<int2*>(const_cast<double*>(ring) + TAB);
+  }
+  __device__ __forceinline__ static bool tabulated(const Args3D& a) { return a.nx * a.ny < (int64_t(1) << 29); }
   // first plane to load: gz (already wrapped)
   __device__ __forceinline__ void setup(const Args3D& a, const double* ring, int x0_, int y0_, int gz) {
     constexpr int R = C::R;
     x0 = x0_;
     y0 = y0_;
     plane = a.u + int64_t(gz) * a.nx * a.ny;
+    if constexpr (!FB) {
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int i = threadIdx.x + k * C::THREADS;
-      off[k] = 0;
-      dst[k] = smem_u32(ring);
-      if (used(k)) {
-        const int r = i / HP, c = 2 * (i - r * HP);
-        const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
-        off[k] = int(gy * a.nx + gx);  // bulk path: nx * ny < 2^31
-        dst[k] = smem_u32(ring + r * C::PITCH + c);
+      for (int k = 0; k < NP; ++k) {
+        const int i = threadIdx.x + k * C::THREADS;
+        off[k] = 0;
+        dst[k] = smem_u32(ring);
+        if (used(k)) {
+          const int r = i / HP, c = 2 * (i - r * HP);
+          const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
+          off[k] = int(gy * a.nx + gx);  // bulk path: nx * ny < 2^31
+          dst[k] = smem_u32(ring + r * C::PITCH + c);
+        }
+      }
+    } else if (tabulated(a)) {
+      int2* t = table(ring);
+      for (int i = threadIdx.x; i < NT; i += C::THREADS) {
+        const int r = i / C::WIDTH, c = i - r * C::WIDTH;
+        double f = 1.0;
+        const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
+        const int o = int(gy * a.nx + gx);
+        t[i] = make_int2(f == 1.0 ? o : (f == 0.0 ? -1 : -2 - o), r * C::PITCH + c);
       }
     }
   }
@@ -196,7 +222,7 @@ struct PlaneLoader {
   // plane (back to z = 0 after the last one: periodic z)
   __device__ __forceinline__ void issue(double* ring, int stage, const Args3D& a, int gz, int gze) {
     constexpr int R = C::R;
-    if (a.bulk_ok) {
+    if constexpr (!FB) {
       const uint32_t soff = uint32_t(stage) * (C::PLANE * 8);
 #pragma unroll
       for (int k = 0; k < NP; ++k)
@@ -208,15 +234,26 @@ struct PlaneLoader {
       double fz = 1.0;
       const int64_t pz = a.z_ghosted ? gze : bc_map(gze, a.nz, a.bc[2], fz);  // gze: the unwrapped plane index
       const double* src = a.u + pz * a.nx * a.ny;
-      for (int i = threadIdx.x; i < C::ROWS * C::WIDTH; i += C::THREADS) {
-        const int r = i / C::WIDTH, c = i - r * C::WIDTH;
-        double f = fz;
-        const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
-        double* d = buf + r * C::PITCH + c;
-        if (f == 1.0)
-          cp_async8(d, src + gy * a.nx + gx);
-        else
-          *d = f == 0.0 ? 0.0 : f * __ldg(src + gy * a.nx + gx);  // boundary zero / odd reflection
+      if (fz == 1.0 && tabulated(a)) {
+        const int2* t = table(ring);
+        for (int i = threadIdx.x; i < NT; i += C::THREADS) {
+          const int2 e = t[i];
+          if (e.x >= 0)
+            cp_async8(buf + e.y, src + e.x);
+          else
+            buf[e.y] = e.x == -1 ? 0.0 : -__ldg(src + (-2 - e.x));  // boundary zero / odd reflection
+        }
+      } else {  // planes mirrored in z (or huge planes): map every element
+        for (int i = threadIdx.x; i < C::ROWS * C::WIDTH; i += C::THREADS) {
+          const int r = i / C::WIDTH, c = i - r * C::WIDTH;
+          double f = fz;
+          const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
+          double* d = buf + r * C::PITCH + c;
+          if (f == 1.0)
+            cp_async8(d, src + gy * a.nx + gx);
+          else
+            *d = f == 0.0 ? 0.0 : f * __ldg(src + gy * a.nx + gx);  // boundary zero / odd reflection
+        }
       }
     }
     plane = (!a.z_ghosted && gz + 1 == a.nz) ? a.u : plane + a.nx * a.ny;
@@ -365,10 +402,10 @@ using CfgChf3T = Cfg3<2, 64, SK_CHT_TY, 2, 2, SK_CHT_S, SK_CHT_MINB>;  // factor
 // Load cursor: walks the block's segment/plane sequence S-1 planes ahead of
 // the compute loop. The per-segment setup (64-bit divisions, wrapped source
 // offsets) is out of line so the unrolled plane loop stays lean.
-template <class C>
+template <class C, bool FB, int TAB = C::STAGES * C::PLANE>
 struct LoadCursor {
   int u, uend, lz, lze, lp, np;  // lz: wrapped plane index, lze: unwrapped (non-periodic z)
-  PlaneLoader<C> ld;
+  PlaneLoader<C, FB, TAB> ld;
   __device__ __forceinline__ void start(const Args3D& a, const double* ring) {
     const Seg seg = seg_of<C>(a, u, uend);
     lze = seg.z0 - C::R;
@@ -391,7 +428,7 @@ struct LoadCursor {
   }
 };
 
-template <Mode M, class C>
+template <Mode M, class C, bool FB>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(const Args3D a) {
   constexpr int R = C::R, Q = C::Q, S = C::STAGES, PX = C::PX, PY = C::PY;
   constexpr int NPT = PX * PY;
@@ -405,7 +442,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
   const int ubeg = b * per + (b < rem ? b : rem);
   const int uend = ubeg + per + (b < rem ? 1 : 0);
 
-  LoadCursor<C> lc;
+  LoadCursor<C, FB> lc;
   lc.u = ubeg;
   lc.uend = uend;
   if (ubeg < uend) lc.start(a, ring);

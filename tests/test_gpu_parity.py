@@ -347,7 +347,7 @@ def test_cg_biharmonic_clamped_vs_oracle(orc, dim, acc, intervals, tol):
 
 
 @pytest.mark.parametrize("dims,steps", [((64, 32, 5), 100), ((128, 64, 6), 230), ((96, 40, 7), 120), ((64, 32, 9), 100),
-                                        ((128, 48), 150)])
+                                        ((128, 48), 150), ((67, 36, 9), 60), ((130, 34, 8), 40)])
 def test_ch_noncubic_grids(orc, dims, steps, monkeypatch):
     # non-cubic periodic grids, tiny z extents (z wrap inside one chunk), the
     # ghost-padded TMA path (whole tiles) and the plain path, vs the oracle
