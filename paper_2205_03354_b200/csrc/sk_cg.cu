@@ -19,6 +19,7 @@
 // iteration count is exact. The rare true-residual check / restart
 // (linalg.cpp:32-47) and the final acceptance test (:59-66) run outside the
 // graph.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,6 +30,7 @@
 #include "sk_internal.hpp"
 #include "sk_cgstate.cuh"
 #include "sk_sell.cuh"
+#include "sk_stencil_kernels.cuh"
 
 namespace sk {
 
@@ -36,7 +38,8 @@ namespace {
 
 constexpr int kT = 256;
 enum : int { kRunning = kCgRunning, kCheck = kCgCheck, kNotPD = kCgNotPD, kMaxIter = kCgMaxIter };
-constexpr int kLoopUnroll = 4;  // CG iterations per round of the device-side while loop (even: see fused2d)
+constexpr int64_t kCoopMaxRows = 131072;  // k_cg2d_coop up to this many unknowns (measured crossover)
+constexpr int kLoopUnroll = 4;  // CG iterations per round of the device-side while loop
 
 // Row i of M times x from the SELL-32 copy (sk_sell.cuh): reference order and rounding.
 template <class IDX>
@@ -227,6 +230,116 @@ __global__ void __launch_bounds__(kT) k_resid(int64_t n, const double* __restric
   }
 }
 
+// Whole CG iterations in one cooperative launch (2D class-1 stencil operator):
+// phase A = the fused apply over the tiles (q = A p', p' = r + beta p, p'.q
+// partials), grid barrier, every CTA sums the partials in the same order
+// (identical alpha everywhere), phase B = the fused update (p = p', x, r,
+// r.r partials), grid barrier, beta and the stopping rule. Runs while the
+// status is RUNNING; CTA 0 publishes the scalars at exit. The recurrence is
+// the fused2d graph path's (same kernels' arithmetic, same reduction order
+// per CTA); L2-resident systems lose the launch and tail gaps of two kernels
+// per iteration.
+using CoopTile = Tile2D<64, 32, 2, 4>;
+
+struct Coop2DArgs {
+  Apply2DArgs a;  // u = p, v = q, r
+  double* x;
+  double* p;
+  double* r;
+  double* part_a;
+  double* part_b;
+  int64_t n;
+  int tiles_x, tiles;
+};
+
+template <int THREADS>
+__device__ __forceinline__ double block_broadcast_sum(const double* partials, int count, double* red, double* slot) {
+  const double v = reduce_partials<THREADS>(partials, count, red);
+  if (threadIdx.x == 0) *slot = v;
+  __syncthreads();
+  return *slot;
+}
+
+__global__ void __launch_bounds__(CoopTile::THREADS, 4) k_cg2d_coop(const Coop2DArgs c, CgState* st) {
+  namespace cg = cooperative_groups;
+  constexpr int T = CoopTile::THREADS;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* tile = reinterpret_cast<double*>(smem_raw + 16);
+  __shared__ double red[32];
+  __shared__ double bcast;
+  double rho = st->rho, beta = st->beta, alpha = st->alpha, pq = st->pq;
+  const double target = st->target;
+  int64_t it = st->it;
+  const int64_t max_iter = st->max_iter;
+  int status = st->status;
+  const int G = gridDim.x;
+  while (status == kRunning) {
+    double acc = 0.0;
+    for (int t = blockIdx.x; t < c.tiles; t += G) {
+      __syncthreads();  // the previous tile is consumed
+      const int ty = t / c.tiles_x, tx = t - ty * c.tiles_x;
+      acc += stencil2d_tile<Mode::CgApply, 64, 32, 2, 4, false>(tile, c.a, int64_t(tx) * 64, int64_t(ty) * 32, beta);
+    }
+    acc = block_sum<T>(acc, red);
+    if (threadIdx.x == 0) c.part_a[blockIdx.x] = acc;
+    grid.sync();
+    pq = block_broadcast_sum<T>(c.part_a, G, red, &bcast);
+    if (pq <= 0) {  // linalg.cpp:50-51
+      status = kNotPD;
+      break;
+    }
+    alpha = rho / pq;
+    const double nalpha = -alpha;
+    acc = 0.0;
+    for (int64_t i = int64_t(blockIdx.x) * T + threadIdx.x; i < c.n; i += int64_t(G) * T) {
+      const double pi = __dadd_rn(c.r[i], __dmul_rn(beta, c.p[i]));  // xpby(r, beta, p)
+      c.p[i] = pi;
+      c.x[i] = __dadd_rn(c.x[i], __dmul_rn(alpha, pi));                 // axpy(alpha, p, x)
+      const double ri = __dadd_rn(c.r[i], __dmul_rn(nalpha, c.a.v[i]));  // axpy(-alpha, q, r)
+      c.r[i] = ri;
+      acc = fma(ri, ri, acc);
+    }
+    acc = block_sum<T>(acc, red);
+    if (threadIdx.x == 0) c.part_b[blockIdx.x] = acc;
+    grid.sync();
+    const double rho_next = block_broadcast_sum<T>(c.part_b, G, red, &bcast);
+    beta = rho_next / rho;
+    rho = rho_next;
+    ++it;
+    if (it >= max_iter) status = kMaxIter;
+    else if (sqrt(rho_next) <= target) status = kCheck;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rho = rho;
+    st->beta = beta;
+    st->alpha = alpha;
+    st->pq = pq;
+    st->it = it;
+    st->status = status;
+  }
+}
+
+// Co-resident grid for k_cg2d_coop (0: cooperative launch unavailable):
+// every SM's resident CTAs, no more than the tiles / rows need.
+int coop_grid_size(int tiles, int64_t n) {
+  int dev = 0, coop = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!coop || sms <= 0) return 0;
+  if (cudaFuncSetAttribute(k_cg2d_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, CoopTile::SMEM_BYTES_CG) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg2d_coop, CoopTile::THREADS,
+                                                    CoopTile::SMEM_BYTES_CG) != cudaSuccess ||
+      per_sm <= 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t need = std::max<int64_t>(tiles, (n + CoopTile::THREADS - 1) / CoopTile::THREADS);
+  return int(std::min<int64_t>(int64_t(per_sm) * sms, need));
+}
+
 }  // namespace
 
 // A CG workspace (r, p, q, partials, device state) plus the captured graph of
@@ -244,6 +357,11 @@ struct CgPlan {
   // fused2d: 2D class-1 stencil operator; each iteration is two kernels,
   // [q = A (r + beta p) ; alpha] and [p = r + beta p ; x, r update ; beta]
   bool fused2d = false;
+  // coop: fused2d iterations run by k_cg2d_coop (one cooperative launch per
+  // round of iterations) instead of the iteration graph
+  bool coop = false;
+  int coop_grid = 0;
+  double* part_b = nullptr;
   cudaGraphExec_t exec = nullptr;
   const double* graph_x = nullptr;
   bool device_loop = false;  // exec = while(status == running) { iteration } on the device
@@ -340,6 +458,24 @@ struct CgPlan {
     graph_x = x;
     return SK_OK;
   }
+  int launch_coop(double* x, cudaStream_t stream) {
+    Coop2DArgs c{};
+    cg_apply_2d_args(op.s, op.g, p, r, q, &c.a);
+    c.x = x;
+    c.p = p;
+    c.r = r;
+    c.part_a = partials;
+    c.part_b = part_b;
+    c.n = n;
+    c.tiles_x = int((op.g.un[0] + 63) / 64);
+    c.tiles = cg_apply_2d_ctas(op.s, op.g);
+    CgState* stp = st;
+    void* args[] = {&c, &stp};
+    SK_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cg2d_coop), dim3(unsigned(coop_grid)),
+                                            dim3(CoopTile::THREADS), args, CoopTile::SMEM_BYTES_CG, stream));
+    SK_LAUNCH_CHECK("k_cg2d_coop");
+    return SK_OK;
+  }
   int iteration(double* x, cudaStream_t cap, bool cond, cudaGraphConditionalHandle h) {
     if (fused2d) {
       if (int e = launch_cg_apply_2d(op.s, op.g, p, r, q, st, partials, cap)) return e;
@@ -409,6 +545,14 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
     if (ctas > 0 && !(env && env[0] == '0')) {
       pl->fused2d = true;
       partials = std::max(partials, ctas);
+      // cooperative kernel for small systems only: measured (tools/cg_fused_timing.py,
+      // config 2's operator) 14.5 vs 16-21 us/iteration at 65k unknowns, but
+      // slower than the two-kernel graph from 261k up (fewer resident CTAs
+      // per phase). SK_CG_COOP=1 / 0 forces it on / off.
+      const char* cenv = getenv("SK_CG_COOP");
+      const bool want = cenv ? cenv[0] == '1' : op.n <= kCoopMaxRows;
+      if (want) pl->coop_grid = coop_grid_size(ctas, op.n);
+      pl->coop = pl->coop_grid > 0;
     }
   }
   if (op.m) {
@@ -418,7 +562,8 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
     }
   }
   const size_t vec = sizeof(double) * size_t(op.n > 0 ? op.n : 1);
-  const size_t ws_bytes = 3 * vec + sizeof(double) * size_t(partials) + sizeof(CgState) + 256;
+  const size_t ws_bytes =
+      3 * vec + sizeof(double) * (size_t(partials) + size_t(pl->coop_grid)) + sizeof(CgState) + 256;
   if (cudaMalloc(reinterpret_cast<void**>(&pl->ws), ws_bytes) != cudaSuccess) {
     delete pl;
     return fail(SK_ERR_OUT_OF_MEMORY, "cg workspace");
@@ -427,7 +572,9 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
   pl->p = pl->r + op.n;
   pl->q = pl->p + op.n;
   pl->partials = pl->q + op.n;
-  pl->st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(pl->partials + partials) + 127) & ~uintptr_t(127));
+  pl->part_b = pl->partials + partials;
+  pl->st = reinterpret_cast<CgState*>((reinterpret_cast<uintptr_t>(pl->part_b + pl->coop_grid) + 127) &
+                                      ~uintptr_t(127));
   *out = pl;
   return SK_OK;
 }
@@ -476,7 +623,8 @@ int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options*
   h.max_iter = max_iter;
   h.status = kRunning;
   SK_CUDA_TRY(cudaMemcpyAsync(s->st, &h, sizeof(CgState), cudaMemcpyHostToDevice, stream));
-  if (int e = s->ensure_graph(x, stream)) return e;
+  if (!s->coop)
+    if (int e = s->ensure_graph(x, stream)) return e;
 
   int64_t restarts = 0;
   double rho = rho0;
@@ -494,13 +642,20 @@ int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options*
       SK_LAUNCH_CHECK("k_restart");
       restarts++;
     }
-    SK_CUDA_TRY(cudaGraphLaunch(s->exec, stream));
+    if (s->coop) {
+      if (int e = s->launch_coop(x, stream)) return e;
+    } else {
+      SK_CUDA_TRY(cudaGraphLaunch(s->exec, stream));
+    }
     SK_CUDA_TRY(cudaMemcpyAsync(&h, s->st, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
     // launched kernels: whole loop bodies up to the round that stopped
     const int64_t rounds = (h.it - it + kLoopUnroll) / kLoopUnroll;
-    g_launches += int64_t(s->kernels_per_iteration()) *
-                  (s->device_loop ? rounds * kLoopUnroll : int64_t(s->check_every));
+    if (s->coop)
+      g_launches += 1;
+    else
+      g_launches += int64_t(s->kernels_per_iteration()) *
+                    (s->device_loop ? rounds * kLoopUnroll : int64_t(s->check_every));
     it = h.it;
     rho = h.rho;
     status = h.status;

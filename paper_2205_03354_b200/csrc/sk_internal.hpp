@@ -76,6 +76,10 @@ struct CgState;
 int cg_apply_2d_ctas(const sk_stencil* s, const GridInfo& g);
 int launch_cg_apply_2d(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
                        CgState* st, double* partials, cudaStream_t stream);
+struct Apply2DArgs;
+// the operator part of the fused apply's arguments (weights, extents, boundary kinds, p, r, q)
+void cg_apply_2d_args(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
+                      Apply2DArgs* out);
 
 // ---- conjugate gradients (sk_cg.cu) ----
 // The operator q = A p: an assembled CSR (SELL SpMV, bit-identical to the

@@ -200,9 +200,8 @@ int cg_apply_2d_ctas(const sk_stencil* s, const GridInfo& g) {
   return int(((g.un[0] + 63) / 64) * ((g.un[1] + SK_T2_TY - 1) / SK_T2_TY));
 }
 
-int launch_cg_apply_2d(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
-                       CgState* st, double* partials, cudaStream_t stream) {
-  if (!cg_apply_2d_ctas(s, g)) return fail(SK_ERR_INVALID_ARGUMENT, "fused CG apply needs a 2D class-1 stencil");
+void cg_apply_2d_args(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
+                      Apply2DArgs* out) {
   const double scale = pow_int(g.h, s->h_power);
   Apply2DArgs a{};
   for (int i = 0; i < 8; ++i) a.w.w[i] = s->orbit_coeff[i] * scale;
@@ -213,6 +212,14 @@ int launch_cg_apply_2d(const sk_stencil* s, const GridInfo& g, const double* p, 
   a.bc[0] = g.bc[0];
   a.bc[1] = g.bc[1];
   a.r = r;
+  *out = a;
+}
+
+int launch_cg_apply_2d(const sk_stencil* s, const GridInfo& g, const double* p, const double* r, double* q,
+                       CgState* st, double* partials, cudaStream_t stream) {
+  if (!cg_apply_2d_ctas(s, g)) return fail(SK_ERR_INVALID_ARGUMENT, "fused CG apply needs a 2D class-1 stencil");
+  Apply2DArgs a{};
+  cg_apply_2d_args(s, g, p, r, q, &a);
   a.st = st;
   a.partials = partials;
   return launch_2d<Mode::CgApply>(a, stream);

@@ -114,15 +114,19 @@ struct Apply2DArgs {
   double* partials;  // one per CTA
 };
 
-template <Mode M, int TX, int TY, int PX, int PY>
-__device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a, int64_t x0, int64_t y0) {
+// NC: p and r are read-only for the whole kernel (ld.global.nc allowed); the
+// cooperative CG kernel, which rewrites them between its grid barriers, loads
+// them coherently (cp.async and ld.global.cg are ordered by the barrier's
+// acquire; the non-coherent read-only path is not).
+template <Mode M, int TX, int TY, int PX, int PY, bool NC = true>
+__device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a, int64_t x0, int64_t y0,
+                                             double beta) {
   using T = Tile2D<TX, TY, PX, PY>;
   constexpr int R = T::R;
   const int tid = threadIdx.x;
   // tile wholly inside the grid: no boundary map
   const bool inner = x0 >= R && x0 + TX + R <= a.nx && y0 >= R && y0 + TY + R <= a.ny;
   if constexpr (M == Mode::CgApply) {
-    const double beta = a.st->beta;
     if (inner) {  // both tiles by 8-byte cp.async, then p' in place (each thread its own points)
       double* rt = tile + T::ROWS * T::PITCH;
       const int64_t base = (y0 - R) * a.nx + (x0 - R);
@@ -142,7 +146,12 @@ __device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a,
       double f = 1.0;
       const int64_t gy = bc_map(y0 - R + r, a.ny, a.bc[1], f), gx = bc_map(x0 - R + c, a.nx, a.bc[0], f);
       const int64_t g = gy * a.nx + gx;
-      tile[i] = f == 0.0 ? 0.0 : f * __dadd_rn(__ldg(a.r + g), __dmul_rn(beta, __ldg(a.u + g)));
+      double v = 0.0;  // boundary zero (g may lie outside the field then)
+      if (f != 0.0) {
+        const double rv = NC ? __ldg(a.r + g) : __ldcg(a.r + g), pv = NC ? __ldg(a.u + g) : __ldcg(a.u + g);
+        v = f * __dadd_rn(rv, __dmul_rn(beta, pv));
+      }
+      tile[i] = v;
     }
     __syncthreads();
   } else if (a.bulk_ok) {
@@ -174,28 +183,14 @@ __device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a,
   }
 }
 
-template <Mode M, int TX, int TY, int PX, int PY>
-__global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
-    stencil2d_kernel(const Apply2DArgs a) {
+// One tile: load (+ halo), evaluate, store. CgApply: returns this thread's
+// p'.q partial (p' = r + beta p). The caller orders the tile buffer's reuse.
+template <Mode M, int TX, int TY, int PX, int PY, bool NC = true>
+__device__ __forceinline__ double stencil2d_tile(double* tile, const Apply2DArgs& a, int64_t x0, int64_t y0,
+                                                 double beta) {
   using T = Tile2D<TX, TY, PX, PY>;
   constexpr int R = T::R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* tile = reinterpret_cast<double*>(smem_raw + 16);
-
-  const int64_t x0 = int64_t(blockIdx.x) * TX, y0 = int64_t(blockIdx.y) * TY;
-  // Programmatic dependent launch (launch_2d): the next kernel of the stream
-  // may start its CTAs now; this one waits for its predecessor before the
-  // first access that can conflict with it: the first load, except for an
-  // Apply whose input no predecessor writes (the repeated apply of config 1),
-  // which loads and computes first and waits before overwriting its output.
-  // Without the launch attribute both instructions are no-ops.
-  asm volatile("griddepcontrol.launch_dependents;");
-  if (M != Mode::Apply || !a.input_stable) asm volatile("griddepcontrol.wait;" ::: "memory");
-  if constexpr (M == Mode::CgApply) {
-    if (a.st->status != kCgRunning) return;  // uniform: set by the previous iteration
-  }
-  __syncthreads();
-  load_tile_2d<M, TX, TY, PX, PY>(tile, a, x0, y0);
+  load_tile_2d<M, TX, TY, PX, PY, NC>(tile, a, x0, y0, beta);
 
   const int tx = threadIdx.x % (TX / PX), ty = threadIdx.x / (TX / PX);
   const int lx = tx * PX + R;  // tile column of the first owned point
@@ -288,6 +283,32 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
         if (gx + i < a.nx) out[i] = val[i];
     }
   }
+  return pq;
+}
+
+template <Mode M, int TX, int TY, int PX, int PY>
+__global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
+    stencil2d_kernel(const Apply2DArgs a) {
+  using T = Tile2D<TX, TY, PX, PY>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* tile = reinterpret_cast<double*>(smem_raw + 16);
+
+  const int64_t x0 = int64_t(blockIdx.x) * TX, y0 = int64_t(blockIdx.y) * TY;
+  // Programmatic dependent launch (launch_2d): the next kernel of the stream
+  // may start its CTAs now; this one waits for its predecessor before the
+  // first access that can conflict with it: the first load, except for an
+  // Apply whose input no predecessor writes (the repeated apply of config 1),
+  // which loads and computes first and waits before overwriting its output
+  // (in stencil2d_tile). Without the launch attribute both are no-ops.
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (M != Mode::Apply || !a.input_stable) asm volatile("griddepcontrol.wait;" ::: "memory");
+  double beta = 0.0;
+  if constexpr (M == Mode::CgApply) {
+    if (a.st->status != kCgRunning) return;  // uniform: set by the previous iteration
+    beta = a.st->beta;
+  }
+  __syncthreads();
+  double pq = stencil2d_tile<M, TX, TY, PX, PY>(tile, a, x0, y0, beta);
   if constexpr (M == Mode::CgApply) {
     __shared__ double red[32];
     const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x, nctas = gridDim.x * gridDim.y;

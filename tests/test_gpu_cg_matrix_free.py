@@ -55,7 +55,7 @@ def test_matrix_free_and_csr_cg_agree_config2():
 
 @pytest.mark.parametrize("bc", [BoundaryKind.clamped, BoundaryKind.simply_supported, BoundaryKind.periodic])
 @pytest.mark.parametrize("check_every", [0, 7])
-def test_fused_2d_iteration_matches_unfused(monkeypatch, bc, check_every):
+def test_fused_2d_iterations_match_unfused(monkeypatch, bc, check_every):
     # the two-kernel 2D iteration (p' = r + beta p on the tile load, p.q in
     # the apply's epilogue) follows the four-kernel one: same recurrence, only
     # the p.q summation order differs. Odd check_every exercises the p / p2
@@ -70,11 +70,16 @@ def test_fused_2d_iteration_matches_unfused(monkeypatch, bc, check_every):
         monkeypatch.setenv("SK_CG_DEVICE_LOOP", "0")  # the unrolled-graph fallback
     reps = []
     xs = []
-    for fused in ("1", "0"):
+    # cooperative kernel (forced), two-kernel graph, four-kernel graph
+    for fused, coop in (("1", "1"), ("1", "0"), ("0", "0")):
         monkeypatch.setenv("SK_CG_FUSED", fused)
+        monkeypatch.setenv("SK_CG_COOP", coop)
         rep = SolveReport()
         xs.append(cg_solve_stencil(DeviceStencil(bilaplacian(2)), g, b, o, rep))  # new stencil -> new plan
         reps.append(rep)
-    assert abs(reps[0].iterations - reps[1].iterations) <= 2
-    assert reps[0].true_rel_residual <= 1e-9
-    assert np.linalg.norm(xs[0] - xs[1]) <= 1e-7 * np.linalg.norm(xs[1])
+    for k in (0, 1):
+        assert abs(reps[k].iterations - reps[2].iterations) <= 2
+        assert reps[k].true_rel_residual <= 1e-9
+        assert np.linalg.norm(xs[k] - xs[2]) <= 1e-7 * np.linalg.norm(xs[2])
+    # the cooperative kernel and the two-kernel graph run the same recurrence
+    assert reps[0].iterations == reps[1].iterations

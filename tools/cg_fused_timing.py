@@ -1,5 +1,5 @@
-"""Matrix-free CG per-iteration time on config 2's clamped biharmonic, fused
-(two-kernel) vs four-kernel 2D iteration. Each variant is timed `reps` times,
+"""Matrix-free CG per-iteration time on config 2's clamped biharmonic: the
+cooperative kernel, the two-kernel and the four-kernel 2D iteration graphs. Each variant is timed `reps` times,
 alternating, and the best is reported (GPU clocks vary run to run).
 
     python tools/cg_fused_timing.py [N ...]
@@ -27,9 +27,11 @@ def main():
         b = np.sin(np.arange(g.unknown_count()) * 0.01) + 1.0
         o = SolveOptions(rel_tol=1e-30, max_iter=iters)
         best = {}
+        variants = {"coop": ("1", "1"), "2k": ("1", "0"), "4k": ("0", "0")}
         for _ in range(reps):
-            for fused in ("1", "0"):
+            for name, (fused, coop) in variants.items():
                 os.environ["SK_CG_FUSED"] = fused
+                os.environ["SK_CG_COOP"] = coop
                 s = DeviceStencil(bilaplacian(2))  # a new plan with this setting (one cached plan per thread)
                 try:
                     cg_solve_stencil(s, g, b, o)  # untimed: plan, graph
@@ -42,9 +44,9 @@ def main():
                 except StencilkitError:
                     pass
                 us = (time.perf_counter() - t) / max(rep.iterations, 1) * 1e6
-                best[fused] = min(best.get(fused, 1e30), us)
-        print(f"N={N} unknowns={g.unknown_count()} fused {best['1']:.2f} us/it  four-kernel {best['0']:.2f} us/it",
-              flush=True)
+                best[name] = min(best.get(name, 1e30), us)
+        print(f"N={N} unknowns={g.unknown_count()} cooperative {best['coop']:.2f} us/it  two-kernel {best['2k']:.2f}"
+              f"  four-kernel {best['4k']:.2f}", flush=True)
 
 
 if __name__ == "__main__":
