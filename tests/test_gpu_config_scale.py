@@ -16,7 +16,7 @@ from paper_2205_03354_b200 import kernels as K  # noqa: E402
 from paper_2205_03354_b200.cahn_hilliard import (CahnHilliardExplicit, CahnHilliardParams, CahnHilliardState,  # noqa: E402
                                                  free_energy)
 from paper_2205_03354_b200.device import DeviceArray  # noqa: E402
-from paper_2205_03354_b200.grid import BoundaryKind, assemble, make_grid, make_periodic_grid  # noqa: E402
+from paper_2205_03354_b200.grid import BoundaryKind, apply, assemble, make_grid, make_periodic_grid  # noqa: E402
 from paper_2205_03354_b200.stencil import bilaplacian  # noqa: E402
 
 
@@ -84,12 +84,21 @@ def test_config5_assembly_sampled_rows_at_257(orc):
     rp = np.empty(m.rows + 1, np.int64)
     from paper_2205_03354_b200._lib import load
 
-    # download only row_ptr; rows are checked through a device SpMV on unit vectors below
+    # download only row_ptr (the entries are 14 GB); the sampled rows' entries
+    # are checked through one device SpMV, which is bit-identical to the
+    # reference's serial csr_matvec: y[r] must equal the oracle row's dot with
+    # x summed in column order with separately rounded multiply and add
     load().sk_csr_download(m.handle, rp.ctypes.data, None, None)
+    x = np.random.default_rng(6).uniform(-1.0, 1.0, m.rows)
+    y = apply(m, x)
     rng = np.random.default_rng(5)
     for r in list(rng.integers(0, m.rows, 200)) + [0, m.rows - 1, 255 * 255 * 128 + 255 * 3 + 1]:
         cols, vals = orc.assemble_row(s, g, int(r))
         assert rp[r + 1] - rp[r] == cols.size
+        acc = 0.0
+        for c, v in zip(cols.tolist(), vals.tolist()):
+            acc += v * x[c]  # Python floats: IEEE double, no contraction
+        assert y[r] == acc, r
     assert rp[-1] == m.nnz()
 
 
