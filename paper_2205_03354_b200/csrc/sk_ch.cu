@@ -22,6 +22,7 @@
 #include "sk_stencil_kernels.cuh"
 #include "sk_stream3d.cuh"
 #include "sk_chf3d.cuh"
+#include "sk_chf3d2.cuh"
 
 namespace sk {
 
@@ -97,6 +98,7 @@ struct ChGraph {
   const void* key_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
   double key_val[17] = {};
   int steps = 0;
+  int64_t launches = 0;  // kernels per replay
   double* pad[2] = {nullptr, nullptr};  // ghost-padded ping-pong fields of the 3D factored path
   size_t pad_elems = 0;
 };
@@ -132,8 +134,9 @@ static CUtensorMapL2promotion l2_promotion() {
                     : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 }
 
-static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo& g) {
-  using CT = CfgChf3T;
+static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo& g,
+                            cuuint32_t box_x = cuuint32_t(ChfSmem<CfgChf3T, 1>::P),
+                            cuuint32_t box_y = cuuint32_t(CfgChf3T::ROWS / kTmaSplit)) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -146,7 +149,7 @@ static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo&
   const cuuint64_t px = cuuint64_t(g.n[0] + 2 * kPadL), py = cuuint64_t(g.n[1] + 2 * kPadT);
   const cuuint64_t dims[3] = {px, py, cuuint64_t(g.n[2])};
   const cuuint64_t strides[2] = {px * 8, px * py * 8};
-  const cuuint32_t box[3] = {cuuint32_t(ChfSmem<CT, 1>::P), cuuint32_t(CT::ROWS / kTmaSplit), 1};
+  const cuuint32_t box[3] = {box_x, box_y, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
@@ -188,6 +191,60 @@ static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
     if (!a.bulk_ok) return launch_chf3d_as<C, V, LD, OUT, true>(a, tm, grid, stream);
   }
   return launch_chf3d_as<C, V, LD, OUT, false>(a, tm, grid, stream);
+}
+
+// Two fused steps (sk_chf3d2.cuh) from a ghost-padded field: OUT 1 into the
+// other padded buffer, OUT 0 into the caller's plain field.
+static bool chf3d2_ok(const GridInfo& g) {
+  // opt-in (SK_CH_2STEP=1): measured slower than single steps on B200 at
+  // 256^3 (97.9 vs 62.6 us/step; the halo-4 frame costs 1.5x the fp64 work
+  // per step and the kernel is issue/latency-bound, ncu in profiles/)
+  const char* e = getenv("SK_CH_2STEP");
+  return chf3d_padded_ok(g) && g.n[2] >= 2 * CfgChf3D2::H + 1 && e && e[0] == '1';
+}
+
+static int ch_two_steps_padded(const sk_stencil* lap, const GridInfo& g, const sk_ch_params* p, double dt,
+                               const double* in, double* out, int out_padded, cudaStream_t stream) {
+  using C = CfgChf3D2;
+  const double dtm = dt * p->mobility, sl = pow_int(g.h, lap->h_power);
+  const double ca = p->c_alpha, cb = p->c_beta, s = ca + cb, pr = ca * cb, r2 = 2.0 * p->rho_w;
+  Args3D a{};
+  a.u = in;
+  a.v = out;
+  a.nx = g.n[0];
+  a.ny = g.n[1];
+  a.nz = g.n[2];
+  a.wl0 = (lap->orbit_coeff[0] * sl) * dtm;
+  a.wl1 = (lap->orbit_coeff[1] * sl) * dtm;
+  a.kl0 = -p->kappa * (lap->orbit_coeff[0] * sl);
+  a.kl1 = -p->kappa * (lap->orbit_coeff[1] * sl);
+  a.chem = Poly3{2.0 * r2, -3.0 * r2 * s, r2 * (s * s + 2.0 * pr), -r2 * pr * s};
+  a.bulk_ok = 1;
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
+  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
+  CUtensorMap tm{};
+  if (int st = make_tmap_padded(&tm, in, g, C::FX, C::FY)) return st;
+  auto kern = out_padded ? chf3d2_kernel<C, 1> : chf3d2_kernel<C, 0>;
+  static const cudaError_t attr1 =
+      cudaFuncSetAttribute(chf3d2_kernel<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  static const cudaError_t attr0 =
+      cudaFuncSetAttribute(chf3d2_kernel<C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  if (attr1 != cudaSuccess) return cuda_fail(attr1, "chf3d2 smem attribute");
+  if (attr0 != cudaSuccess) return cuda_fail(attr0, "chf3d2 smem attribute");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  const char* env = getenv("SK_PDL");
+  cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
+  SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, tm));
+  SK_LAUNCH_CHECK("chf3d2_kernel");
+  return SK_OK;
 }
 
 // One fused step on the fast path (in -> out).
@@ -313,12 +370,13 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
     const char* env_pad = getenv("SK_CH_PADDED");
     const bool padded = g.dim == 3 && p->formulation != SK_CH_COMPOSED && ptr_ok && chf3d_padded_ok(g) &&
                         !(env_pad && env_pad[0] == '0');
+    const bool two = padded && chf3d2_ok(g) && p->formulation == SK_CH_FACTORED;
     const double key_val[17] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
                                 double(g.n[0]), double(g.n[1]), double(g.n[2]),
                                 double(g.dim) + 10.0 * double(p->formulation),
                                 lap->orbit_coeff[0], lap->orbit_coeff[1], bilap->orbit_coeff[0],
                                 bilap->orbit_coeff[1], bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3],
-                                double(padded)};
+                                double(padded) + 2.0 * double(two)};
     const void* key_ptr[4] = {c, scratch, lap, bilap};
     bool hit = g_ch_graph.exec != nullptr;
     for (int i = 0; i < 4 && hit; ++i) hit = key_ptr[i] == g_ch_graph.key_ptr[i];
@@ -344,7 +402,17 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
       cudaStream_t cap = stream ? stream : capture_stream();
       SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       int st = SK_OK;
-      for (int k = 0; k < kGraphSteps && st == SK_OK; ++k) {
+      const int64_t l0 = g_launches.load();
+      // 3D padded chunks: single step into the padded field, 2-step launches
+      // (sk_chf3d2.cuh) pad -> pad, single step back into c (kGraphSteps even)
+      if (two) {
+        st = ch_step_fast(lap, bilap, g, p, dt, c, pad[0], cap, ptr_ok, kIoFirst);
+        int cur = 0;
+        for (int k = 1; k + 1 < kGraphSteps && st == SK_OK; k += 2, cur ^= 1)
+          st = ch_two_steps_padded(lap, g, p, dt, pad[cur], pad[cur ^ 1], 1, cap);
+        if (st == SK_OK) st = ch_step_fast(lap, bilap, g, p, dt, pad[cur], c, cap, ptr_ok, kIoLast);
+      }
+      for (int k = 0; k < kGraphSteps && st == SK_OK && !two; ++k) {
         if (!padded)
           st = ch_step_fast(lap, bilap, g, p, dt, (k % 2) ? scratch : c, (k % 2) ? c : scratch, cap, ptr_ok);
         else if (k == 0)
@@ -366,11 +434,12 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
       for (int i = 0; i < 4; ++i) g_ch_graph.key_ptr[i] = key_ptr[i];
       for (int i = 0; i < 17; ++i) g_ch_graph.key_val[i] = key_val[i];
-      g_launches -= kGraphSteps;  // capture does not execute; counted per replay below
+      g_ch_graph.launches = g_launches.load() - l0;
+      g_launches -= g_ch_graph.launches;  // capture does not execute; counted per replay below
     }
     for (int64_t k = 0; k < full; k += kGraphSteps) {
       SK_CUDA_TRY(cudaGraphLaunch(g_ch_graph.exec, stream));
-      g_launches += kGraphSteps;
+      g_launches += g_ch_graph.launches;
     }
   }
   for (int64_t k = full; k < nsteps; ++k) {

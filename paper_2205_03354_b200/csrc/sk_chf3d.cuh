@@ -42,11 +42,11 @@ namespace sk {
 // Ghost-padded field of the TMA path: row pitch nx + 2 kPadL, kPadT ghost
 // rows above and below; interior x at column x + kPadL (128 B-aligned rows
 // and tiles, so the interior stores are whole lines), ghosts x = -2, -1 and
-// nx, nx + 1 at columns kPadL - 2 .. and kPadL + nx ...
+// nx, nx + 1 at columns kPadL - 2 .. and kPadL + nx ... (images: 4 columns, 4 rows)
 #ifndef SK_PADL
 #define SK_PADL 16
 #endif
-constexpr int kPadL = SK_PADL, kPadT = 2;
+constexpr int kPadL = SK_PADL, kPadT = 4;  // 4 ghost rows: the 2-step kernel's boxes (sk_chf3d2.cuh)
 // L2 policy of the TMA loads: evict_last keeps tile halos for the
 // y-neighbour tile's CTA (measured +0.5%; evict_first: -19%)
 #ifndef SK_TMA_HINT
@@ -208,9 +208,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
     const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
     double* outp = a.v + int64_t(sg.z0) * opp + (gy0 + (OUT ? kPadT : 0)) * opx + gx0 + (OUT ? kPadL : 0);
     // OUT 1: periodic images in the ghost frame: columns 0..3 and nx-4..nx-1
-    // (whole 32 B sectors: no partial-sector writes), rows 0, 1 and ny-2, ny-1
+    // (whole 32 B sectors: no partial-sector writes), rows 0..3 and ny-4..ny-1
     const int64_t gdx_ = OUT ? (gx0 < 4 ? a.nx : (gx0 >= a.nx - 4 ? -a.nx : 0)) : 0;
-    const int64_t gdy_ = OUT ? (gy0 == 0 ? a.ny : (gy0 == a.ny - 2 ? -a.ny : 0)) * opx : 0;
+    const int64_t gdy_ = OUT ? (gy0 < 4 ? a.ny : (gy0 >= a.ny - 4 ? -a.ny : 0)) * opx : 0;
 #ifdef SK_NO_GHOST  // timing experiment only (wrong results)
     const int64_t gdx = 0 * gdx_, gdy = 0 * gdy_;
 #else
@@ -275,11 +275,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         if (lane == 0) { lf0 = cb[-1]; lf1 = cb[P - 1]; }
         if (lane == 31) { rt0 = cb[2]; rt1 = cb[P + 2]; }
         const double2 up = ld2(cb - P), dn = ld2(cb + 2 * P);
-        // 6-neighbour sums: ((z-1 + z+1) + (left + right)) + (up + down)
-        const double s00 = ((zm[0] + zp[0]) + (lf0 + c1[1])) + (up.x + c1[2]);
-        const double s01 = ((zm[1] + zp[1]) + (c1[0] + rt0)) + (up.y + c1[3]);
-        const double s10 = ((zm[2] + zp[2]) + (lf1 + c1[3])) + (c1[0] + dn.x);
-        const double s11 = ((zm[3] + zp[3]) + (c1[2] + rt1)) + (c1[1] + dn.y);
+        // 6-neighbour sums: (((left + right) + (up + down)) + z-1) + z+1 (the
+        // plane that arrived last enters last: short dependency chains)
+        const double s00 = (((lf0 + c1[1]) + (up.x + c1[2])) + zm[0]) + zp[0];
+        const double s01 = (((c1[0] + rt0) + (up.y + c1[3])) + zm[1]) + zp[1];
+        const double s10 = (((lf1 + c1[3]) + (c1[0] + dn.x)) + zm[2]) + zp[2];
+        const double s11 = (((c1[2] + rt1) + (c1[1] + dn.y)) + zm[3]) + zp[3];
         double* m1 = M[M1];
         m1[0] = fma(a.kl1, s00, fma(a.kl0, c1[0], poly3(c1[0], a.chem)));
         m1[1] = fma(a.kl1, s01, fma(a.kl0, c1[1], poly3(c1[1], a.chem)));
@@ -299,10 +300,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           const double* m1 = M[M1];
           const double* m2 = M[M2];
           const double* m3 = M[M3];
-          const double s00 = ((m3[0] + m1[0]) + (olf0 + m2[1])) + (oup.x + m2[2]);
-          const double s01 = ((m3[1] + m1[1]) + (m2[0] + ort0)) + (oup.y + m2[3]);
-          const double s10 = ((m3[2] + m1[2]) + (olf1 + m2[3])) + (m2[0] + odn.x);
-          const double s11 = ((m3[3] + m1[3]) + (m2[2] + ort1)) + (m2[1] + odn.y);
+          const double s00 = (((olf0 + m2[1]) + (oup.x + m2[2])) + m3[0]) + m1[0];
+          const double s01 = (((m2[0] + ort0) + (oup.y + m2[3])) + m3[1]) + m1[1];
+          const double s10 = (((olf1 + m2[3]) + (m2[0] + odn.x)) + m3[2]) + m1[2];
+          const double s11 = (((m2[2] + ort1) + (m2[1] + odn.y)) + m3[3]) + m1[3];
           o[0] = fma(a.wl1, s00, fma(a.wl0, m2[0], c2[0]));
           o[1] = fma(a.wl1, s01, fma(a.wl0, m2[1], c2[1]));
           o[2] = fma(a.wl1, s10, fma(a.wl0, m2[2], c2[2]));
@@ -339,8 +340,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         if (has_ex) {  // one border point of the mu tile (needed from the next step on)
           const double* rb = ring + s_k1 * PLANE + ex_c;
           const double cc = rb[0];
-          const double sr = ((ring[s_k2 * PLANE + ex_c] + ring[s_k * PLANE + ex_c]) + (rb[-1] + rb[1])) +
-                            (rb[-P] + rb[P]);
+          const double sr =
+              (((rb[-1] + rb[1]) + (rb[-P] + rb[P])) + ring[s_k2 * PLANE + ex_c]) + ring[s_k * PLANE + ex_c];
           mu_ring[M1 * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
         }
       }
