@@ -7,6 +7,7 @@ __graft_entry__.py / paper_2205_03354_b200.build_ext compiles it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 from typing import Optional
 
@@ -111,10 +112,13 @@ def load() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
-        raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+    # SK_LIB_AB: an alternative in-tree build under _ab/ (same-box A/B timing of kernel variants)
+    ab = os.environ.get("SK_LIB_AB")
+    path = (LIB_PATH.parent.parent / "_ab" / ab) if ab else LIB_PATH
+    if not path.exists():
+        raise RuntimeError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                            "(the CUDA path has no CPU fallback)")
-    lib = C.CDLL(str(LIB_PATH))
+    lib = C.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

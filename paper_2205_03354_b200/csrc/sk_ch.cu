@@ -121,7 +121,8 @@ enum ChfIo { kIoPlain = 0, kIoFirst = 1, kIoMid = 2, kIoLast = 3 };  // in/out: 
 // up to ~21M points (320^3 = 32.8M: padded 134 us, plain faster).
 static bool chf3d_padded_ok(const GridInfo& g) {
   using CT = CfgChf3T;
-  return g.dim == 3 && g.n[0] % CT::TX == 0 && g.n[1] % CT::TY == 0 &&
+  // whole tiles of both the TMA kernel and the first step's cp.async kernel (CfgChf3: OUT 1)
+  return g.dim == 3 && g.n[0] % CT::TX == 0 && g.n[1] % CT::TY == 0 && g.n[1] % CfgChf3::TY == 0 &&
          (g.n[0] + 2 * kPadL) * (g.n[1] + 2 * kPadT) < (int64_t(1) << 31) && g.rows <= (int64_t(5) << 22);
 }
 
@@ -182,6 +183,9 @@ static int launch_chf3d_as(const Args3D& a, const CUtensorMap& tm, int64_t grid,
 
 template <class C, int V, int LD, int OUT>
 static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
+  // TMA steps (inside graph chunks): rotated, phase-aligned columns (seg_of)
+  const char* zr = getenv("SK_ZROT");  // experiments: 0 = z-chunk schedule
+  a.zrot = (LD == 1 && !a.z_ghosted && !(zr && zr[0] == '0')) ? 1 : 0;
   // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
@@ -250,7 +254,7 @@ static int ch_two_steps_padded(const sk_stencil* lap, const GridInfo& g, const s
 // One fused step on the fast path (in -> out).
 static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
                         double dt, const double* in, double* out, cudaStream_t stream, bool bulk_ok_ptrs,
-                        int io = kIoPlain, bool z_ghosted = false) {
+                        int io = kIoPlain, bool z_ghosted = false, int ghost = 2) {
   const double dtm = dt * p->mobility;
   const double fac_b = -dtm * p->kappa;
   const double sb = pow_int(g.h, bilap->h_power), sl = pow_int(g.h, lap->h_power);
@@ -288,6 +292,7 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   a.chem = chem;
   a.bulk_ok = bulk_ok_ptrs && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R;
   a.z_ghosted = z_ghosted ? 1 : 0;
+  a.ghost = ghost;
   if (p->formulation == SK_CH_COMPOSED) return launch_3d<Mode::CahnHilliard, C3R2>(a, stream);
   // factored: mu = f' - kappa L c ; c' = c + dt M L mu
   a.kl0 = -p->kappa * (lap->orbit_coeff[0] * sl);
@@ -406,7 +411,7 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
       // 3D padded chunks: single step into the padded field, 2-step launches
       // (sk_chf3d2.cuh) pad -> pad, single step back into c (kGraphSteps even)
       if (two) {
-        st = ch_step_fast(lap, bilap, g, p, dt, c, pad[0], cap, ptr_ok, kIoFirst);
+        st = ch_step_fast(lap, bilap, g, p, dt, c, pad[0], cap, ptr_ok, kIoFirst, false, CfgChf3D2::H);
         int cur = 0;
         for (int k = 1; k + 1 < kGraphSteps && st == SK_OK; k += 2, cur ^= 1)
           st = ch_two_steps_padded(lap, g, p, dt, pad[cur], pad[cur ^ 1], 1, cap);

@@ -52,6 +52,9 @@ constexpr int kPadL = SK_PADL, kPadT = 4;  // 4 ghost rows: the 2-step kernel's 
 #ifndef SK_TMA_HINT
 #define SK_TMA_HINT 1
 #endif
+#ifndef SK_MU_SLOTS
+#define SK_MU_SLOTS 3
+#endif
 #ifndef SK_TMA_SPLIT
 #define SK_TMA_SPLIT 1
 #endif
@@ -74,8 +77,9 @@ struct ChfSmem {
   static constexpr int MP = C::TX + 4;              // mu ring pitch: x in [-1, TX] at column x + 2
   static constexpr int MU_ROWS = C::TY + 2;         // y in [-1, TY]
   static constexpr int MU_PLANE = MU_ROWS * MP;
+  static constexpr int MU_SLOTS = SK_MU_SLOTS;     // 2: slot parity (written at step k, read at k+1)
   // LD 0 with the 8-byte fallback loader (FB): its boundary-map table after the mu ring
-  static constexpr int TAB = C::STAGES * PLANE + 3 * MU_PLANE;  // doubles from the ring
+  static constexpr int TAB = C::STAGES * PLANE + MU_SLOTS * MU_PLANE;  // doubles from the ring
   static constexpr int BYTES = RING_OFS + TAB * 8 + (FB ? C::TABLE_BYTES : 0);
   static constexpr int WARPS = C::THREADS / 32;
   static constexpr int BORDER_ROWS = 2 * (C::TX + 2);                     // mu rows -1 and TY, x in [-1, TX]
@@ -200,6 +204,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   double Cz[3][4], M[3][4];  // own c of plane j in Cz[j % 3], own mu of plane j in M[j % 3]; point 2 * row + col
   int s_k = 0;               // stage of c-plane k
   uint32_t ph = 0;           // LD 1: parity of the current use of stage s_k
+  int mpar = 0;              // MU_SLOTS 2: mu slot of plane k-1
   for (int u = ubeg; u < uend; ) {
     const Seg sg = seg_of<C>(a, u, uend);
     u += sg.len;
@@ -208,9 +213,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
     const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
     double* outp = a.v + int64_t(sg.z0) * opp + (gy0 + (OUT ? kPadT : 0)) * opx + gx0 + (OUT ? kPadL : 0);
     // OUT 1: periodic images in the ghost frame: columns 0..3 and nx-4..nx-1
-    // (whole 32 B sectors: no partial-sector writes), rows 0..3 and ny-4..ny-1
+    // (whole 32 B sectors: no partial-sector writes), rows 0..g-1 and ny-g..ny-1
+    // (g = a.ghost: 2, or 4 when a 2-step launch reads the field)
     const int64_t gdx_ = OUT ? (gx0 < 4 ? a.nx : (gx0 >= a.nx - 4 ? -a.nx : 0)) : 0;
-    const int64_t gdy_ = OUT ? (gy0 < 4 ? a.ny : (gy0 >= a.ny - 4 ? -a.ny : 0)) * opx : 0;
+    const int64_t gdy_ = OUT ? (gy0 < a.ghost ? a.ny : (gy0 >= a.ny - a.ghost ? -a.ny : 0)) * opx : 0;
 #ifdef SK_NO_GHOST  // timing experiment only (wrong results)
     const int64_t gdx = 0 * gdx_, gdy = 0 * gdy_;
 #else
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       double2 oup = make_double2(0, 0), odn = make_double2(0, 0);
       if constexpr (DO_OUT && V == 0) {
         const double* m2 = M[M2];
-        const double* mb = mu_ring + M2 * SM::MU_PLANE + mofs;  // slot of plane k-2
+        const double* mb = mu_ring + (SM::MU_SLOTS == 2 ? (mpar ^ 1) : M2) * SM::MU_PLANE + mofs;  // plane k-2
         olf0 = __shfl_up_sync(0xffffffffu, m2[1], 1);
         olf1 = __shfl_up_sync(0xffffffffu, m2[3], 1);
         ort0 = __shfl_down_sync(0xffffffffu, m2[0], 1);
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         m1[1] = fma(a.kl1, s01, fma(a.kl0, c1[1], poly3(c1[1], a.chem)));
         m1[2] = fma(a.kl1, s10, fma(a.kl0, c1[2], poly3(c1[2], a.chem)));
         m1[3] = fma(a.kl1, s11, fma(a.kl0, c1[3], poly3(c1[3], a.chem)));
-        double* mb = mu_ring + M1 * SM::MU_PLANE + mofs;  // slot of plane k-1
+        double* mb = mu_ring + (SM::MU_SLOTS == 2 ? mpar : M1) * SM::MU_PLANE + mofs;  // plane k-1
         *reinterpret_cast<double2*>(mb) = make_double2(m1[0], m1[1]);
         *reinterpret_cast<double2*>(mb + MP) = make_double2(m1[2], m1[3]);
       }
@@ -342,13 +348,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           const double cc = rb[0];
           const double sr =
               (((rb[-1] + rb[1]) + (rb[-P] + rb[P])) + ring[s_k2 * PLANE + ex_c]) + ring[s_k * PLANE + ex_c];
-          mu_ring[M1 * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
+          mu_ring[(SM::MU_SLOTS == 2 ? mpar : M1) * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
         }
       }
       if (++s_k == S) {
         s_k = 0;
         ph ^= 1u;
       }
+      mpar ^= 1;
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
