@@ -113,17 +113,16 @@ constexpr int kGraphSteps = 100;  // kernels per captured graph (even: buffers r
 // the first loads one TMA box per plane without wrap logic.
 enum ChfIo { kIoPlain = 0, kIoFirst = 1, kIoMid = 2, kIoLast = 3 };  // in/out: plain/plain, plain/pad, pad/pad, pad/plain
 
-// whole tiles of the TMA kernel, even padded rows (16 B strides), int32 in-plane offsets
-// Measured crossover (tools/kbench.py ch3d --n N, 100-step chunks): the padded
-// TMA path wins at 256^3 (61.6 vs 65.7 us) and loses from 384^3 up (its
-// ghost-frame stores and the padded output stream cost more than the wrap
-// logic it saves: 384^3 221 vs 208 us, 1024^3 4.46 vs 4.05 ms), so it is used
-// up to ~21M points (320^3 = 32.8M: padded 134 us, plain faster).
+// whole tiles of the TMA kernel, even padded rows (16 B strides), int32 in-plane offsets.
+// Measured (tools/kbench.py ch3d --n N, 100-step chunks, padded vs plain
+// cp.async path): 256^3 57.2 vs 68.3 us, 384^3 184 vs 211 us, 512^3 444 vs
+// 505 us. (Before the rotated-column schedule and 64x16 tiles the padded path
+// lost from 384^3 up and was limited to ~21M points.)
 static bool chf3d_padded_ok(const GridInfo& g) {
   using CT = CfgChf3T;
   // whole tiles of both the TMA kernel and the first step's cp.async kernel (CfgChf3: OUT 1)
   return g.dim == 3 && g.n[0] % CT::TX == 0 && g.n[1] % CT::TY == 0 && g.n[1] % CfgChf3::TY == 0 &&
-         (g.n[0] + 2 * kPadL) * (g.n[1] + 2 * kPadT) < (int64_t(1) << 31) && g.rows <= (int64_t(5) << 22);
+         (g.n[0] + 2 * kPadL) * (g.n[1] + 2 * kPadT) < (int64_t(1) << 31);
 }
 
 static CUtensorMapL2promotion l2_promotion() {

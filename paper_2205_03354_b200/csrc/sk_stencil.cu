@@ -179,9 +179,12 @@ int launch_3d(Args3D a, cudaStream_t stream) {
   constexpr int bulk_smem = C::SMEM_BYTES - C::TABLE_BYTES;  // no boundary-map table
   static int once = set_smem(bulk, bulk_smem) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, C::SMEM_BYTES);
   if (once != SK_OK) return once;
-  // lockstep for the radius-2 apply (halo rows from L2), balanced for the
-  // issue-bound radius-4 apply and the composed CH step (measured at 256^3)
-  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/C::R == 2 && M == Mode::Apply);
+  // rotated columns (seg_of: balanced ranges, neighbour tiles in phase);
+  // SK_ZROT=0: lockstep for the radius-2 apply (halo rows from L2), balanced
+  // for the issue-bound radius-4 apply and the composed CH step
+  const char* zr = getenv("SK_ZROT");
+  a.zrot = (!a.z_ghosted && !(zr && zr[0] == '0')) ? 1 : 0;
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/!a.zrot && C::R == 2 && M == Mode::Apply);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   if (a.bulk_ok)  // (after persistent_grid, which may clear it)
     bulk<<<unsigned(grid), C::THREADS, bulk_smem, stream>>>(a);

@@ -64,3 +64,12 @@ def test_two_step_config4_grid(monkeypatch):
     out, _ = run((256, 256, 256), 200, {k: MODES[k] for k in ("two", "one")}, monkeypatch, seed=2)
     assert np.array_equal(out["two"], out["one"])
     assert np.isfinite(out["two"]).all()
+
+
+@pytest.mark.parametrize("dims,steps", [((384, 384, 384), 100), ((512, 256, 64), 100)])
+def test_padded_large_grids(dims, steps, monkeypatch):
+    # the ghost-padded TMA path at any size (rotated-column schedule, 64x16
+    # tiles): bit-identical to the plain cp.async path
+    out, _ = run(dims, steps, {k: MODES[k] for k in ("one", "plain")}, monkeypatch, seed=5)
+    assert np.array_equal(out["one"], out["plain"])
+    assert np.isfinite(out["one"]).all()
