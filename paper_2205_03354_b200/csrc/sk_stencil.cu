@@ -17,6 +17,7 @@
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
 #include "sk_stream3d.cuh"
+#include "sk_fac3d.cuh"
 
 sk_stencil::~sk_stencil() {
   if (rep_exec) cudaGraphExecDestroy(rep_exec);
@@ -268,6 +269,40 @@ static bool streamable(const sk_stencil* s, const GridInfo& g, int radius) {
   return true;
 }
 
+// The uploaded stencil is compose(laplacian(3, 4), laplacian(3, 4)) (the
+// 73-point composition of configs 5's operator, stencil.cpp:75-87): orbit
+// coefficients 1607/24, -182/9, 32/9, 109/36, -2/9, 1/72, -2/9, 1/144 (as the
+// reference's truncated doubles, within 2 ulp) and h^-4.
+static bool is_l4l4(const sk_stencil* s) {
+  if (s->kclass != 3 || s->dim != 3 || s->h_power != -4) return false;
+  static const double want[8] = {1607.0 / 24, -182.0 / 9, 32.0 / 9, 109.0 / 36, -2.0 / 9, 1.0 / 72, -2.0 / 9, 1.0 / 144};
+  for (int i = 0; i < 8; ++i)
+    if (!(std::fabs(s->orbit_coeff[i] - want[i]) <= 4.5e-16 * std::fabs(want[i]))) return false;
+  return true;
+}
+
+// Factored 73-point apply (sk_fac3d.cuh): L4 weights (centre 3 * -30/12,
+// axis +-1: 16/12, axis +-2: -1/12, generators.cpp:98) scaled by h^-2 per pass.
+static int launch_fac73(Args3D a, double h_m2, cudaStream_t stream) {
+  using C = CfgFac73;
+  using SM = FacSmem<C>;
+  const L4W lw{(3.0 * (-30.0 / 12.0)) * h_m2, (16.0 / 12.0) * h_m2, (-1.0 / 12.0) * h_m2};
+  auto bulk = fac73_kernel<C, false>;
+  auto fallback = fac73_kernel<C, true>;
+  static int once = set_smem(bulk, SM::BYTES) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, SM::BYTES_FB);
+  if (once != SK_OK) return once;
+  const char* zr = getenv("SK_ZROT");
+  a.zrot = !(zr && zr[0] == '0') ? 1 : 0;
+  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
+  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
+  if (a.bulk_ok)
+    bulk<<<unsigned(grid), C::THREADS, SM::BYTES, stream>>>(a, lw);
+  else
+    fallback<<<unsigned(grid), C::THREADS, SM::BYTES_FB, stream>>>(a, lw);
+  SK_LAUNCH_CHECK("fac73_kernel");
+  return SK_OK;
+}
+
 int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream,
                  bool input_stable) {
   const double scale = pow_int(g.h, s->h_power);
@@ -303,6 +338,11 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     }
     a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
                 aligned16(u) && aligned16(v);
+    if (per && is_l4l4(s)) {  // B = compose(L4, L4) on a periodic grid: two fused L4 passes possible
+      // opt-in (SK_F73=1): measured slower than the literal kernel (sk_fac3d.cuh, Status)
+      const char* e = getenv("SK_F73");
+      if (e && e[0] == '1') return launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
+    }
     return launch_3d<Mode::Apply, C3R4>(a, stream);
   }
   return launch_generic(s, g, u, v, stream);
