@@ -365,7 +365,8 @@ struct CgPlan {
   cudaGraphExec_t exec = nullptr;
   const double* graph_x = nullptr;
   bool device_loop = false;  // exec = while(status == running) { iteration } on the device
-  int kernels_per_iteration() const { return fused2d ? 2 : (op.m ? 3 : 4); }
+  bool pq_fused = false;     // 3D streaming stencil: the apply reduces p.q itself
+  int kernels_per_iteration() const { return fused2d ? 2 : ((op.m || pq_fused) ? 3 : 4); }
 
   ~CgPlan() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -387,6 +388,8 @@ struct CgPlan {
       SK_LAUNCH_CHECK("k1_spmv_pq");
       return SK_OK;
     }
+    const int f = launch_apply_pq(op.s, op.g, p, q, st, partials, stream);  // fused p.q (3D streaming stencils)
+    if (f != kApplyPqUnsupported) return f;
     if (int e = launch_apply(op.s, op.g, p, q, stream)) return e;
     k_pq<<<grid, kT, 0, stream>>>(n, p, q, st, partials);
     SK_LAUNCH_CHECK("k_pq");
@@ -540,6 +543,8 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
   pl->grid = int(g > int64_t(kNumSMs) * 8 ? int64_t(kNumSMs) * 8 : (g > 0 ? g : 1));
   int partials = pl->grid;
   if (op.s) {
+    pl->pq_fused = apply_pq_supported(op.s, op.g);
+    partials = std::max(partials, kNumSMs * 4);  // the 3D streaming apply's persistent grid (fused p.q)
     const char* env = getenv("SK_CG_FUSED");
     const int ctas = cg_apply_2d_ctas(op.s, op.g);
     if (ctas > 0 && !(env && env[0] == '0')) {

@@ -28,7 +28,7 @@ namespace sk {
 
 template <Mode M>
 int launch_2d(const Apply2DArgs& a, cudaStream_t stream);
-template <Mode M, class C>
+template <Mode M, class C, bool PQ = false>
 int launch_3d(Args3D a, cudaStream_t stream);
 using C3R2 = Cfg3CH;
 

@@ -65,6 +65,11 @@ int check_width(const sk_stencil* s, const GridInfo& g);
 // Launch one matrix-free application on `stream` (device pointers).
 // input_stable: u is not written by the kernel launched just before, so the
 // 2D kernel may load it before its programmatic-launch wait.
+struct CgState;
+constexpr int kApplyPqUnsupported = -1;
+bool apply_pq_supported(const sk_stencil* s, const GridInfo& g);
+int launch_apply_pq(const sk_stencil* s, const GridInfo& g, const double* p, double* q, CgState* st,
+                    double* partials, cudaStream_t stream);
 int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double* v, cudaStream_t stream,
                  bool input_stable = false);
 

@@ -173,10 +173,12 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
   return SK_OK;
 }
 
-template <Mode M, class C>
+template <Mode M, class C, bool PQ = false>
+int launch_3d(Args3D a, cudaStream_t stream);
+template <Mode M, class C, bool PQ>
 int launch_3d(Args3D a, cudaStream_t stream) {
-  auto bulk = stream3d_kernel<M, C, false>;
-  auto fallback = stream3d_kernel<M, C, true>;
+  auto bulk = stream3d_kernel<M, C, false, PQ>;
+  auto fallback = stream3d_kernel<M, C, true, PQ>;
   constexpr int bulk_smem = C::SMEM_BYTES - C::TABLE_BYTES;  // no boundary-map table
   static int once = set_smem(bulk, bulk_smem) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, C::SMEM_BYTES);
   if (once != SK_OK) return once;
@@ -346,6 +348,40 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     return launch_3d<Mode::Apply, C3R4>(a, stream);
   }
   return launch_generic(s, g, u, v, stream);
+}
+
+// Matrix-free CG: q = A p fused with p.q -> alpha (stream3d_kernel<..., PQ>)
+// for the 3D streaming stencils; kApplyPqUnsupported: the caller runs the
+// apply and a separate p.q pass. SK_CG_PQ=0 disables it.
+bool apply_pq_supported(const sk_stencil* s, const GridInfo& g) {
+  const char* env = getenv("SK_CG_PQ");
+  return !(env && env[0] == '0') && g.dim == 3 && (s->kclass == 2 || s->kclass == 3) &&
+         streamable(s, g, s->kclass == 2 ? 2 : 4);
+}
+
+int launch_apply_pq(const sk_stencil* s, const GridInfo& g, const double* p, double* q, CgState* st,
+                    double* partials, cudaStream_t stream) {
+  if (!apply_pq_supported(s, g)) return kApplyPqUnsupported;
+  const double scale = pow_int(g.h, s->h_power);
+  const bool per = all_periodic(g);
+  Args3D a{};
+  a.u = p;
+  a.v = q;
+  a.nx = g.un[0];
+  a.ny = g.un[1];
+  a.nz = g.un[2];
+  for (int i = 0; i < 3; ++i) a.bc[i] = g.bc[i];
+  for (int i = 0; i < 8; ++i) a.w[i] = s->orbit_coeff[i] * scale;
+  a.cg = st;
+  a.cg_partials = partials;
+  if (s->kclass == 2) {
+    a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R &&
+                aligned16(p) && aligned16(q);
+    return launch_3d<Mode::Apply, C3R2, true>(a, stream);
+  }
+  a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
+              aligned16(p) && aligned16(q);
+  return launch_3d<Mode::Apply, C3R4, true>(a, stream);
 }
 
 }  // namespace sk

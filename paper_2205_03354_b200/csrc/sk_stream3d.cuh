@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "sk_cgstate.cuh"
 #include "sk_common.cuh"
 #include "sk_stencil_kernels.cuh"
 
@@ -71,6 +72,8 @@ struct Args3D {
   int bulk_ok;       // even nx, tiles fit, aligned, nx*ny < 2^31: 16-byte copies, int32 offsets
   int bc[3];         // boundary kind per axis (nx, ny, nz are unknown counts); bulk path: periodic only
   int z_ghosted;     // slab mode: planes -R..-1 and nz..nz+R-1 exist in memory around u (no z wrap)
+  CgState* cg;       // PQ kernels (matrix-free CG, sk_cg.cu): q = A p fused with p.q -> alpha
+  double* cg_partials;
   int zchunk;        // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
   int ghost;         // chf3d OUT 1: ghost rows written on each side (2; 4 when a 2-step launch reads them)
   int zrot;          // periodic z, zchunk = nz: every tile column is rotated so CTA range starts sit at
@@ -466,10 +469,20 @@ struct LoadCursor {
   }
 };
 
-template <Mode M, class C, bool FB>
+// PQ (Apply only): one matrix-free CG iteration's q = A p (sk_cg.cu) with the
+// p.q reduction in the store epilogue (p re-read from L2 at the output point)
+// and alpha = rho / p.q (or "not positive definite") published by the last
+// CTA: the separate p.q pass (16 B per unknown) disappears. A no-op once the
+// solver has stopped, like the other kernels of the iteration graph.
+template <Mode M, class C, bool FB, bool PQ = false>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(const Args3D a) {
   constexpr int R = C::R, Q = C::Q, S = C::STAGES, PX = C::PX, PY = C::PY;
   constexpr int NPT = PX * PY;
+  if constexpr (PQ) {
+    if (a.cg->status != kCgRunning) return;
+  }
+  double pq = 0.0;
+  (void)pq;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw + C::RING_OFS);
 
@@ -556,6 +569,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
                 for (int i = 0; i < PX; ++i)
                   if (gx0 + i < a.nx) dst[i] = val[i];
               }
+              if constexpr (PQ) {
+                const double* pp = a.u + (dst - a.v);
+#pragma unroll
+                for (int i = 0; i < PX; ++i)
+                  if (gx0 + i < a.nx) pq = fma(__ldg(pp + i), val[i], pq);
+              }
             }
             outp += plane_sz;
           }
@@ -565,6 +584,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
     u += sg.len;
   }
   cp_async_wait_all();
+  if constexpr (PQ) {
+    __shared__ double sh[32];
+    pq = block_sum<C::THREADS>(pq, sh);
+    if (threadIdx.x == 0) a.cg_partials[blockIdx.x] = pq;
+    if (last_block(&a.cg->counter[0])) {
+      const double t = reduce_partials<C::THREADS>(a.cg_partials, gridDim.x, sh);
+      if (threadIdx.x == 0) cg_publish_pq(a.cg, t);
+    }
+  }
 }
 
 }  // namespace sk
