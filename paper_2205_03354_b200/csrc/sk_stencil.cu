@@ -355,8 +355,9 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
 // apply and a separate p.q pass. SK_CG_PQ=0 disables it.
 bool apply_pq_supported(const sk_stencil* s, const GridInfo& g) {
   const char* env = getenv("SK_CG_PQ");
-  return !(env && env[0] == '0') && g.dim == 3 && (s->kclass == 2 || s->kclass == 3) &&
-         streamable(s, g, s->kclass == 2 ? 2 : 4);
+  // radius 2 only: the radius-4 kernel (234+ registers) slows down with the
+  // epilogue (config 5 matrix-free: 0.457 -> 0.494 ms per iteration)
+  return !(env && env[0] == '0') && g.dim == 3 && s->kclass == 2 && streamable(s, g, 2);
 }
 
 int launch_apply_pq(const sk_stencil* s, const GridInfo& g, const double* p, double* q, CgState* st,
@@ -374,14 +375,9 @@ int launch_apply_pq(const sk_stencil* s, const GridInfo& g, const double* p, dou
   for (int i = 0; i < 8; ++i) a.w[i] = s->orbit_coeff[i] * scale;
   a.cg = st;
   a.cg_partials = partials;
-  if (s->kclass == 2) {
-    a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R &&
-                aligned16(p) && aligned16(q);
-    return launch_3d<Mode::Apply, C3R2, true>(a, stream);
-  }
-  a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
+  a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R2::TX + 2 * C3R2::R && a.ny >= C3R2::TY + 2 * C3R2::R &&
               aligned16(p) && aligned16(q);
-  return launch_3d<Mode::Apply, C3R4, true>(a, stream);
+  return launch_3d<Mode::Apply, C3R2, true>(a, stream);
 }
 
 }  // namespace sk

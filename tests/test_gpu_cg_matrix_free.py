@@ -83,3 +83,27 @@ def test_fused_2d_iterations_match_unfused(monkeypatch, bc, check_every):
         assert np.linalg.norm(xs[k] - xs[2]) <= 1e-7 * np.linalg.norm(xs[2])
     # the cooperative kernel and the two-kernel graph run the same recurrence
     assert reps[0].iterations == reps[1].iterations
+
+
+@pytest.mark.parametrize("bc", [BoundaryKind.clamped, BoundaryKind.simply_supported, BoundaryKind.periodic])
+@pytest.mark.parametrize("check_every", [0, 7])
+def test_3d_apply_pq_matches_separate_pass(monkeypatch, bc, check_every):
+    # 3D radius-2 stencils: p.q reduced in the streaming apply's epilogue
+    # (three kernels per iteration) follows the separate p.q pass: same
+    # recurrence, only the p.q summation order differs
+    N = 24
+    g = make_grid(3, N + 1, 1.0 / N, bc)
+    b = np.sin(np.arange(g.unknown_count()) * 0.013) + (0.0 if bc == BoundaryKind.periodic else 1.0)
+    b -= b.mean() if bc == BoundaryKind.periodic else 0.0
+    o = SolveOptions(rel_tol=1e-9, check_every=check_every, deflate_mean=bc == BoundaryKind.periodic)
+    if check_every:
+        monkeypatch.setenv("SK_CG_DEVICE_LOOP", "0")
+    reps, xs = [], []
+    for pq in ("1", "0"):
+        monkeypatch.setenv("SK_CG_PQ", pq)
+        rep = SolveReport()
+        xs.append(cg_solve_stencil(DeviceStencil(bilaplacian(3)), g, b, o, rep))
+        reps.append(rep)
+    assert abs(reps[0].iterations - reps[1].iterations) <= 2
+    assert reps[0].true_rel_residual <= 1e-9
+    assert np.linalg.norm(xs[0] - xs[1]) <= 1e-7 * np.linalg.norm(xs[1])
