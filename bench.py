@@ -176,12 +176,19 @@ class Events:
         return float(ms.value)
 
 
-def ncu_traffic(kernel_key: str):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+def ncu_traffic(kernel_key: str, steady: bool = False):
+    """dram bytes per launch from the committed ncu summary, if any: the one
+    `--set full` launch (cold L2: writes still dirty in L2 at the end are not
+    counted), or with steady=True consecutive launches under
+    `--cache-control none` (the L2 state a step really starts from)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     try:
-        d = json.loads(p.read_text())
-        v = d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        d = json.loads(p.read_text()).get(kernel_key, {})
+        if steady:
+            ss = d.get("steady_state", {})
+            v = ss.get("dram_read_bytes", 0) + ss.get("dram_write_bytes", 0)
+        else:
+            v = d.get("dram_bytes_per_launch")
         return float(v) if v else None
     except Exception:
         return None
@@ -603,6 +610,7 @@ def main() -> int:
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy read+write)", "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(kernel),
+                     "traffic_steady_state": ncu_traffic(kernel, steady=True),
                      "algorithmic_bytes_per_launch": bytes_step},
     }
     if "e2e_s" in r:
