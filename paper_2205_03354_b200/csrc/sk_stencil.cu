@@ -345,6 +345,8 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
       const char* e = getenv("SK_F73");
       if (e && e[0] == '1') return launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
     }
+    if (a.bulk_ok && a.nx >= Cfg3R4P::TX + 2 * Cfg3R4P::R && a.ny >= Cfg3R4P::TY + 2 * Cfg3R4P::R)
+      return launch_3d<Mode::Apply, Cfg3R4P>(a, stream);
     return launch_3d<Mode::Apply, C3R4>(a, stream);
   }
   return launch_generic(s, g, u, v, stream);

@@ -428,6 +428,17 @@ using Cfg3CH = Cfg3<2, 64, SK_CH3_TY, 2, 2, SK_CH3_S, SK_CH3_MINB>;    // 3D CH 
 #define SK_A73_MINB 1
 #endif
 using Cfg3R4 = Cfg3<4, 64, SK_A73_TY, SK_A73_PX, SK_A73_PY, SK_A73_S, SK_A73_MINB>;    // 73-point apply
+// 73-point apply on the 16-byte (periodic) path: 64x8 tiles, 10 stages, 2
+// CTAs/SM — with the rotated-column schedule the extra halo rows come from
+// L2, and two independent CTAs per SM hide each other's barrier: 108.6 ->
+// 96.9 us at 256^3. The boundary-mapped loader (clamped / simply supported)
+// keeps 64x16 x 1 CTA (its per-segment table favours big tiles: 204 vs 241 us).
+#ifndef SK_A73P_TY
+#define SK_A73P_TY 8
+#define SK_A73P_S 10
+#define SK_A73P_MINB 2
+#endif
+using Cfg3R4P = Cfg3<4, 64, SK_A73P_TY, 2, 2, SK_A73P_S, SK_A73P_MINB>;
 using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
 #ifndef SK_CHT_TY
 // 64x16 tiles, 7 stages, 2 CTAs/SM (with the rotated-column schedule the
