@@ -3,14 +3,16 @@
 //
 // Work decomposition: the grid is cut into TX x TY column tiles; the unit of
 // work is one OUTPUT PLANE of one tile. The tiles*nz units are split into
-// gridDim.x contiguous, equal ranges (one persistent CTA per SM: a single
-// balanced wave); a range walks z inside a tile and may continue into the
-// next tile (a new "segment", whose first 2R planes re-prime the pipeline).
+// gridDim.x contiguous, equal ranges (MIN_BLOCKS persistent CTAs per SM: a
+// single balanced wave); a range walks z inside a tile and may continue into
+// the next tile (a new "segment", whose first 2R planes re-prime the
+// pipeline). With Args3D::zrot the tile columns are rotated in z so that all
+// CTAs stream the same planes at the same time (seg_of).
 //
-// Pipeline: one producer warp streams input planes ((TY+2R) x (TX+2R)
-// doubles, periodic wrap = <= 2 TMA bulk copies per row) into a STAGES-deep
-// shared-memory ring with full/empty mbarriers; 8 consumer warps evaluate the
-// stencil. Each consumer thread owns PX x PY points and, per input plane:
+// Pipeline: every thread issues its share of each input plane ((TY+2R) x
+// (TX+2R) doubles, periodic wrap or boundary map: PlaneLoader) as cp.async
+// into a STAGES-deep shared-memory ring, STAGES-1 planes ahead; one barrier
+// per plane. Each thread owns PX x PY points and, per input plane:
 //   1. loads the (PY+2R) rows of its window as 128-bit shared loads,
 //   2. accumulates in-plane ORBIT SUMS (centre, A1 = 4 axis neighbours at 1,
 //      D11 = 4 diagonals, A2, and for R=4 D21, D22, A3, A4) — the first member
