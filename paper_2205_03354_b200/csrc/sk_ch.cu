@@ -182,9 +182,9 @@ static int launch_chf3d_as(const Args3D& a, const CUtensorMap& tm, int64_t grid,
 
 template <class C, int V, int LD, int OUT>
 static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
-  // TMA steps (inside graph chunks): rotated, phase-aligned columns (seg_of)
+  // rotated, phase-aligned columns (seg_of); not for slabs (z_ghosted)
   const char* zr = getenv("SK_ZROT");  // experiments: 0 = z-chunk schedule
-  a.zrot = (LD == 1 && !a.z_ghosted && !(zr && zr[0] == '0')) ? 1 : 0;
+  a.zrot = (!a.z_ghosted && !(zr && zr[0] == '0')) ? 1 : 0;
   // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");

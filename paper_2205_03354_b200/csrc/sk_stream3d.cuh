@@ -441,7 +441,12 @@ using Cfg3R4 = Cfg3<4, 64, SK_A73_TY, SK_A73_PX, SK_A73_PY, SK_A73_S, SK_A73_MIN
 #define SK_A73P_MINB 2
 #endif
 using Cfg3R4P = Cfg3<4, 64, SK_A73P_TY, 2, 2, SK_A73P_S, SK_A73P_MINB>;
-using CfgChf3 = Cfg3<2, 64, 32, 2, 2, 6, 1>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
+#ifndef SK_CHP_TY  // cp.async path (first step of a chunk, remainders, grids without whole TMA tiles):
+#define SK_CHP_TY 16  // 64x16 tiles, 2 CTAs/SM + rotated columns: 68.3 -> 65.2 us/step at 256^3
+#define SK_CHP_S 6
+#define SK_CHP_MINB 2
+#endif
+using CfgChf3 = Cfg3<2, 64, SK_CHP_TY, 2, 2, SK_CHP_S, SK_CHP_MINB>;   // factored 3D CH (sk_chf3d.cuh), cp.async loads
 #ifndef SK_CHT_TY
 // 64x16 tiles, 7 stages, 2 CTAs/SM (with the rotated-column schedule the
 // halo rows come from L2, so smaller tiles cost little and two CTAs hide
