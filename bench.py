@@ -251,9 +251,8 @@ def run_ch(lib, dim: int, steps: int, warmup: int, d: Dist, e2e: bool = True, fo
         lib.sk_host_register(host.ctypes.data, host.nbytes)
         from paper_2205_03354_b200.cahn_hilliard import CahnHilliardState
 
-        st = CahnHilliardState(g, host)
-        stepper.step(st, dt, 1)  # warm the host path
-        st.c = host
+        st = CahnHilliardState(g, host.copy())
+        stepper.step(st, dt, steps)  # warm the host path: its staging buffers and chunk graphs (not timed)
         d.barrier()
         t0 = time.perf_counter()
         from paper_2205_03354_b200._lib import check
@@ -542,7 +541,7 @@ def ref_ch_steps_per_s(dim: int, steps: int, warmup: int):
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["ch3d", "ch2d"], default="ch3d")

@@ -130,6 +130,9 @@ int sk_device_free(void* p);
 int sk_memcpy_h2d(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 int sk_memcpy_d2h(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 int sk_stream_sync(void* stream);
+/* A non-blocking stream for callers without their own CUDA runtime. */
+int sk_stream_create(void** out);
+int sk_stream_destroy(void* stream);
 /* Host-side seeded input: std::mt19937_64(seed) + uniform_real_distribution<double>(lo, hi),
  * drawn in order — the generator the reference uses (linalg.cpp:77-78). */
 int sk_fill_uniform_host(uint64_t seed, int64_t count, double lo, double hi, double* out);
@@ -145,6 +148,27 @@ int sk_event_record(void* ev, void* stream);
 int sk_event_elapsed_ms(void* start, void* end, float* ms); /* waits for `end` */
 /* Evict L2 by writing a buffer larger than it (timing hygiene). */
 int sk_l2_flush(void* stream);
+
+/* ---- execution options ----------------------------------------------------
+ * Process-wide switches between alternative device paths that compute the
+ * same result (kept for parity tests and A/B timing). They are set only
+ * through this call — the library never reads the environment — and every
+ * cached graph or plan is rebuilt after a change. Defaults are the measured
+ * fastest paths. Unknown options or values:
+ * SK_ERR_INVALID_ARGUMENT. */
+enum sk_option {
+  SK_OPT_PDL = 0,              /* programmatic dependent launch between chained kernels: 1 */
+  SK_OPT_CH_PADDED = 1,        /* 3D factored CH runs >= 2 steps through ghost-padded TMA buffers: 1 */
+  SK_OPT_CG_DEVICE_LOOP = 2,   /* CG iterations in a device-side while loop (0: unrolled graph chunks): 1 */
+  SK_OPT_CG_FUSED = 3,         /* 2D matrix-free CG: two-kernel fused iteration: 1 */
+  SK_OPT_CG_COOP = 4,          /* 2D matrix-free CG, one cooperative kernel per iteration: -1 auto, 0, 1 */
+  SK_OPT_CG_PQ = 5,            /* 3D radius-2 matrix-free CG: p.q reduced in the apply epilogue: 1 */
+  SK_OPT_IMEX_MATRIX_FREE = 6, /* IMEX implicit operator applied matrix-free (0: CSR SpMV): 1 */
+  SK_OPT_APPLY73_FACTORED = 7, /* periodic 73-point apply as L4(L4 u) (0: literal 73 weights): 0 */
+  SK_OPT_COUNT = 8
+};
+int sk_set_option(int option, int value);
+int sk_get_option(int option, int* value);
 
 /* ---- stencil (host composition result -> device) ------------------------
  * Replaces handing a `stencilkit::Stencil` (stencil.hpp:19-42) to assemble().

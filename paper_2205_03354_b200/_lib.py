@@ -7,7 +7,6 @@ __graft_entry__.py / paper_2205_03354_b200.build_ext compiles it.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from pathlib import Path
 from typing import Optional
 
@@ -55,6 +54,8 @@ SIGNATURES = {
     "sk_memcpy_h2d": (c_int, [vp, vp, C.c_size_t, vp]),
     "sk_memcpy_d2h": (c_int, [vp, vp, C.c_size_t, vp]),
     "sk_stream_sync": (c_int, [vp]),
+    "sk_stream_create": (c_int, [C.POINTER(vp)]),
+    "sk_stream_destroy": (c_int, [vp]),
     "sk_fill_uniform_host": (c_int, [C.c_uint64, c_i64, c_dbl, c_dbl, vp]),
     "sk_launch_count": (c_i64, []),
     "sk_host_register": (c_int, [vp, C.c_size_t]),
@@ -64,6 +65,8 @@ SIGNATURES = {
     "sk_event_record": (c_int, [vp, vp]),
     "sk_event_elapsed_ms": (c_int, [vp, vp, C.POINTER(C.c_float)]),
     "sk_l2_flush": (c_int, [vp]),
+    "sk_set_option": (c_int, [c_int, c_int]),
+    "sk_get_option": (c_int, [c_int, C.POINTER(c_int)]),
     "sk_stencil_create": (c_int, [c_int, c_int, vp, vp, c_int, C.POINTER(vp)]),
     "sk_stencil_destroy": (c_int, [vp]),
     "sk_stencil_kernel_class": (c_int, [vp]),
@@ -107,14 +110,14 @@ SIGNATURES = {
 _lib: Optional[C.CDLL] = None
 
 
-def load() -> C.CDLL:
-    """Load libsk_cuda.so and declare every signature. Raises if it is absent."""
+def load(path: Optional[Path] = None) -> C.CDLL:
+    """Load libsk_cuda.so and declare every signature. Raises if it is absent.
+
+    `path` (tools only): an explicitly named alternative build of the same ABI."""
     global _lib
     if _lib is not None:
         return _lib
-    # SK_LIB_AB: an alternative in-tree build under _ab/ (same-box A/B timing of kernel variants)
-    ab = os.environ.get("SK_LIB_AB")
-    path = (LIB_PATH.parent.parent / "_ab" / ab) if ab else LIB_PATH
+    path = Path(path) if path is not None else LIB_PATH
     if not path.exists():
         raise RuntimeError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                            "(the CUDA path has no CPU fallback)")
@@ -125,6 +128,37 @@ def load() -> C.CDLL:
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+# sk_set_option ids (include/sk_cuda.h enum sk_option)
+OPTIONS = {"pdl": 0, "ch_padded": 1, "cg_device_loop": 2, "cg_fused": 3, "cg_coop": 4, "cg_pq": 5,
+           "imex_matrix_free": 6, "apply73_factored": 7}
+
+
+def set_option(name: str, value: int) -> int:
+    """Set one execution option (explicit; the library never reads the environment); returns the old value."""
+    lib = load()
+    old = c_int()
+    check(lib.sk_get_option(OPTIONS[name], C.byref(old)))
+    check(lib.sk_set_option(OPTIONS[name], int(value)))
+    return old.value
+
+
+class options:
+    """Context manager: `with options(ch_padded=0): ...` restores the previous values on exit."""
+
+    def __init__(self, **kw: int):
+        self.kw = kw
+        self.saved: dict = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.saved[k] = set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_option(k, v)
 
 
 def check(status: int) -> None:

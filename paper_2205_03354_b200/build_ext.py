@@ -46,8 +46,7 @@ def _newest_input() -> float:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = BUILD / (Path(src).stem + ".o")
-    extra = os.environ.get("SK_NVCC_EXTRA", "").split()  # experiments, e.g. "-DSK_TMA_SPLIT=2"
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
+    cmd = [nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")

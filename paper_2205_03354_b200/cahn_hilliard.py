@@ -43,7 +43,7 @@ class CahnHilliardParams:
         p = ChParams()
         p.kappa, p.mobility, p.rho_w, p.c_alpha, p.c_beta = (self.kappa, self.mobility, self.rho_w, self.c_alpha,
                                                               self.c_beta)
-        codes = {"factored": 0, "composed": 1, "probe-copy": 2}  # probe-copy: data-movement ceiling, not a CH step
+        codes = {"factored": 0, "composed": 1}
         if self.formulation not in codes:
             raise StencilkitError(Errc.invalid_argument, f"unknown CH formulation '{self.formulation}'")
         p.formulation = codes[self.formulation]

@@ -436,8 +436,7 @@ struct CgPlan {
       exec = nullptr;
     }
     cudaStream_t cap = stream ? stream : capture_stream();
-    const char* env = getenv("SK_CG_DEVICE_LOOP");
-    if (!(env && env[0] == '0') && build_loop_graph(x, cap) == SK_OK) {
+    if (option(SK_OPT_CG_DEVICE_LOOP) && build_loop_graph(x, cap) == SK_OK) {
       device_loop = true;
       graph_x = x;
       return SK_OK;
@@ -545,17 +544,16 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
   if (op.s) {
     pl->pq_fused = apply_pq_supported(op.s, op.g);
     partials = std::max(partials, kNumSMs * 4);  // the 3D streaming apply's persistent grid (fused p.q)
-    const char* env = getenv("SK_CG_FUSED");
     const int ctas = cg_apply_2d_ctas(op.s, op.g);
-    if (ctas > 0 && !(env && env[0] == '0')) {
+    if (ctas > 0 && option(SK_OPT_CG_FUSED)) {
       pl->fused2d = true;
       partials = std::max(partials, ctas);
       // cooperative kernel for small systems only: measured (tools/cg_fused_timing.py,
       // config 2's operator) 14.5 vs 16-21 us/iteration at 65k unknowns, but
       // slower than the two-kernel graph from 261k up (fewer resident CTAs
-      // per phase). SK_CG_COOP=1 / 0 forces it on / off.
-      const char* cenv = getenv("SK_CG_COOP");
-      const bool want = cenv ? cenv[0] == '1' : op.n <= kCoopMaxRows;
+      // per phase). SK_OPT_CG_COOP 1 / 0 forces it on / off.
+      const int coop = option(SK_OPT_CG_COOP);
+      const bool want = coop >= 0 ? coop == 1 : op.n <= kCoopMaxRows;
       if (want) pl->coop_grid = coop_grid_size(ctas, op.n);
       pl->coop = pl->coop_grid > 0;
     }
@@ -709,12 +707,13 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
   struct Cache {
     uint64_t uid = 0;
     int check_every = -1;
+    uint64_t epoch = 0;
     CgPlan* plan = nullptr;
     ~Cache() { cg_plan_destroy(plan); }
   };
   thread_local Cache cache;
   const int ce = o ? o->check_every : 0;
-  if (!cache.plan || cache.uid != m->uid || cache.check_every != ce) {
+  if (!cache.plan || cache.uid != m->uid || cache.check_every != ce || cache.epoch != option_epoch()) {
     if (cache.plan) {
       cudaDeviceSynchronize();  // the old workspace may still be in use by queued work
       cg_plan_destroy(cache.plan);
@@ -726,6 +725,7 @@ int cg_solve(const sk_csr* m, const double* b, double* x, const sk_solve_options
     if (int e = cg_plan_create(op, ce, stream, &cache.plan)) return e;
     cache.uid = m->uid;
     cache.check_every = ce;
+    cache.epoch = option_epoch();
   }
   return cg_plan_solve(cache.plan, b, x, o, rep, stream);
 }
@@ -741,12 +741,14 @@ int cg_solve_stencil(const sk_stencil* s, const GridInfo& g, const double* b, do
     uint64_t uid = 0;
     GridInfo g{};
     int check_every = -1;
+    uint64_t epoch = 0;
     CgPlan* plan = nullptr;
     ~Cache() { cg_plan_destroy(plan); }
   };
   thread_local Cache cache;
   const int ce = o ? o->check_every : 0;
-  bool hit = cache.plan && cache.uid == s->uid && cache.check_every == ce && cache.g.dim == g.dim && cache.g.h == g.h;
+  bool hit = cache.plan && cache.uid == s->uid && cache.check_every == ce && cache.g.dim == g.dim &&
+             cache.g.h == g.h && cache.epoch == option_epoch();
   for (int a = 0; a < 3 && hit; ++a) hit = cache.g.n[a] == g.n[a] && cache.g.bc[a] == g.bc[a];
   if (!hit) {
     if (cache.plan) {
@@ -762,6 +764,7 @@ int cg_solve_stencil(const sk_stencil* s, const GridInfo& g, const double* b, do
     cache.uid = s->uid;
     cache.g = g;
     cache.check_every = ce;
+    cache.epoch = option_epoch();
   }
   return cg_plan_solve(cache.plan, b, x, o, rep, stream);
 }

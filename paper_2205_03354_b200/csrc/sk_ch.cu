@@ -17,12 +17,12 @@
 #include <cmath>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
 #include "sk_stream3d.cuh"
 #include "sk_chf3d.cuh"
-#include "sk_chf3d2.cuh"
 
 namespace sk {
 
@@ -92,19 +92,7 @@ bool is_lap_shape(const sk_stencil* s, int dim) {
 
 bool is_bilap_shape(const sk_stencil* s, int dim) { return s->kclass == (dim == 2 ? 1 : 2); }
 
-struct ChGraph {
-  std::mutex mu;
-  cudaGraphExec_t exec = nullptr;
-  const void* key_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
-  double key_val[17] = {};
-  int steps = 0;
-  int64_t launches = 0;  // kernels per replay
-  double* pad[2] = {nullptr, nullptr};  // ghost-padded ping-pong fields of the 3D factored path
-  size_t pad_elems = 0;
-};
-ChGraph g_ch_graph;
-
-constexpr int kGraphSteps = 100;  // kernels per captured graph (even: buffers return to start)
+constexpr int kGraphSteps = 100;  // steps per full chunk graph (even: buffers return to start)
 
 }  // namespace
 
@@ -125,15 +113,6 @@ static bool chf3d_padded_ok(const GridInfo& g) {
          (g.n[0] + 2 * kPadL) * (g.n[1] + 2 * kPadT) < (int64_t(1) << 31);
 }
 
-static CUtensorMapL2promotion l2_promotion() {
-  const char* e = getenv("SK_TMA_L2");  // experiments: 0 (none) / 64 / 128 / 256
-  const int v = e ? atoi(e) : 64;  // 64 B promotion: measured +1.6% at 256^3, +10% at 1024^3
-  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-         : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-}
-
 static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo& g,
                             cuuint32_t box_x = cuuint32_t(ChfSmem<CfgChf3T, 1>::P),
                             cuuint32_t box_y = cuuint32_t(CfgChf3T::ROWS / kTmaSplit)) {
@@ -152,7 +131,8 @@ static int make_tmap_padded(CUtensorMap* tm, const double* base, const GridInfo&
   const cuuint32_t box[3] = {box_x, box_y, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
-                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_64B,  // measured +1.6% at 256^3, +10% at 1024^3
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return SK_OK;
@@ -173,8 +153,7 @@ static int launch_chf3d_as(const Args3D& a, const CUtensorMap& tm, int64_t grid,
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap launch with the previous step
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  const char* env = getenv("SK_PDL");
-  cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
+  cfg.numAttrs = option(SK_OPT_PDL) ? 1 : 0;
   SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, tm));
   SK_LAUNCH_CHECK("chf3d_kernel");
   return SK_OK;
@@ -183,8 +162,7 @@ static int launch_chf3d_as(const Args3D& a, const CUtensorMap& tm, int64_t grid,
 template <class C, int V, int LD, int OUT>
 static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
   // rotated, phase-aligned columns (seg_of); not for slabs (z_ghosted)
-  const char* zr = getenv("SK_ZROT");  // experiments: 0 = z-chunk schedule
-  a.zrot = (!a.z_ghosted && !(zr && zr[0] == '0')) ? 1 : 0;
+  a.zrot = a.z_ghosted ? 0 : 1;
   // balanced static schedule (measured faster than lockstep z-chunks at 256^3)
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
@@ -194,60 +172,6 @@ static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
     if (!a.bulk_ok) return launch_chf3d_as<C, V, LD, OUT, true>(a, tm, grid, stream);
   }
   return launch_chf3d_as<C, V, LD, OUT, false>(a, tm, grid, stream);
-}
-
-// Two fused steps (sk_chf3d2.cuh) from a ghost-padded field: OUT 1 into the
-// other padded buffer, OUT 0 into the caller's plain field.
-static bool chf3d2_ok(const GridInfo& g) {
-  // opt-in (SK_CH_2STEP=1): measured slower than single steps on B200 at
-  // 256^3 (97.9 vs 62.6 us/step; the halo-4 frame costs 1.5x the fp64 work
-  // per step and the kernel is issue/latency-bound, ncu in profiles/)
-  const char* e = getenv("SK_CH_2STEP");
-  return chf3d_padded_ok(g) && g.n[2] >= 2 * CfgChf3D2::H + 1 && e && e[0] == '1';
-}
-
-static int ch_two_steps_padded(const sk_stencil* lap, const GridInfo& g, const sk_ch_params* p, double dt,
-                               const double* in, double* out, int out_padded, cudaStream_t stream) {
-  using C = CfgChf3D2;
-  const double dtm = dt * p->mobility, sl = pow_int(g.h, lap->h_power);
-  const double ca = p->c_alpha, cb = p->c_beta, s = ca + cb, pr = ca * cb, r2 = 2.0 * p->rho_w;
-  Args3D a{};
-  a.u = in;
-  a.v = out;
-  a.nx = g.n[0];
-  a.ny = g.n[1];
-  a.nz = g.n[2];
-  a.wl0 = (lap->orbit_coeff[0] * sl) * dtm;
-  a.wl1 = (lap->orbit_coeff[1] * sl) * dtm;
-  a.kl0 = -p->kappa * (lap->orbit_coeff[0] * sl);
-  a.kl1 = -p->kappa * (lap->orbit_coeff[1] * sl);
-  a.chem = Poly3{2.0 * r2, -3.0 * r2 * s, r2 * (s * s + 2.0 * pr), -r2 * pr * s};
-  a.bulk_ok = 1;
-  const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
-  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
-  CUtensorMap tm{};
-  if (int st = make_tmap_padded(&tm, in, g, C::FX, C::FY)) return st;
-  auto kern = out_padded ? chf3d2_kernel<C, 1> : chf3d2_kernel<C, 0>;
-  static const cudaError_t attr1 =
-      cudaFuncSetAttribute(chf3d2_kernel<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
-  static const cudaError_t attr0 =
-      cudaFuncSetAttribute(chf3d2_kernel<C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
-  if (attr1 != cudaSuccess) return cuda_fail(attr1, "chf3d2 smem attribute");
-  if (attr0 != cudaSuccess) return cuda_fail(attr0, "chf3d2 smem attribute");
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::BYTES;
-  cfg.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  const char* env = getenv("SK_PDL");
-  cfg.numAttrs = (env && env[0] == '0') ? 0 : 1;
-  SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, tm));
-  SK_LAUNCH_CHECK("chf3d2_kernel");
-  return SK_OK;
 }
 
 // One fused step on the fast path (in -> out).
@@ -298,20 +222,132 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   a.kl1 = -p->kappa * (lap->orbit_coeff[1] * sl);
   using CF = CfgChf3;
   using CT = CfgChf3T;
-  const bool probe = p->formulation == 2;  // data-movement probe (profiling)
   CUtensorMap tm{};
   if (io == kIoMid || io == kIoLast)
     if (int st = make_tmap_padded(&tm, in, g)) return st;
   switch (io) {
-    case kIoFirst:
-      return probe ? launch_chf3d<CF, 1, 0, 1>(a, tm, stream) : launch_chf3d<CF, 0, 0, 1>(a, tm, stream);
-    case kIoMid:
-      return probe ? launch_chf3d<CT, 1, 1, 1>(a, tm, stream) : launch_chf3d<CT, 0, 1, 1>(a, tm, stream);
-    case kIoLast:
-      return probe ? launch_chf3d<CT, 1, 1, 0>(a, tm, stream) : launch_chf3d<CT, 0, 1, 0>(a, tm, stream);
-    default:
-      return probe ? launch_chf3d<CF, 1, 0, 0>(a, tm, stream) : launch_chf3d<CF, 0, 0, 0>(a, tm, stream);
+    case kIoFirst: return launch_chf3d<CF, 0, 0, 1>(a, tm, stream);
+    case kIoMid: return launch_chf3d<CT, 0, 1, 1>(a, tm, stream);
+    case kIoLast: return launch_chf3d<CT, 0, 1, 0>(a, tm, stream);
+    default: return launch_chf3d<CF, 0, 0, 0>(a, tm, stream);
   }
+}
+
+// ---- chunk graphs --------------------------------------------------------
+// nsteps >= 2 run as chunks of at most kGraphSteps (+1 for the last) steps,
+// each one cached CUDA graph. A plain chunk ping-pongs c <-> scratch; a
+// padded chunk (3D factored, whole tiles) runs c -> pad -> ... -> pad -> out
+// through two ghost-padded buffers, so every step but the first loads its
+// tile planes with one TMA box and no wrap logic. Every chunk starts from c;
+// all but the last end in c; the last ends where the ping-pong parity says
+// (result_is_scratch = nsteps % 2).
+//
+// The padded buffers belong to the launch stream: chunks replayed on one
+// stream are stream-ordered, so they may share a pair; chunks on different
+// streams never do. Graphs are keyed by everything their kernels bake in.
+struct ChKey {
+  double v[16] = {};
+  uint64_t lap_uid = 0, bilap_uid = 0, epoch = 0;
+  const void* c = nullptr;
+  const void* scratch = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t len = 0;
+  int padded = 0, to_scratch = 0;
+  bool operator==(const ChKey& o) const {
+    for (int i = 0; i < 16; ++i)
+      if (v[i] != o.v[i]) return false;
+    return lap_uid == o.lap_uid && bilap_uid == o.bilap_uid && epoch == o.epoch && c == o.c &&
+           scratch == o.scratch && stream == o.stream && len == o.len && padded == o.padded &&
+           to_scratch == o.to_scratch;
+  }
+};
+
+struct ChChunk {
+  ChKey key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;  // kernels per replay
+  uint64_t used = 0;
+};
+
+struct ChPads {
+  cudaStream_t stream = nullptr;
+  size_t elems = 0;
+  double* pad[2] = {nullptr, nullptr};
+  uint64_t used = 0;
+};
+
+struct ChCache {
+  std::mutex mu;
+  std::vector<ChChunk> chunks;
+  std::vector<ChPads> pads;
+  uint64_t tick = 0;
+  static constexpr size_t kMaxChunks = 16, kMaxPads = 2;
+  ~ChCache() {  // process exit: the context may already be gone; do not touch the device
+    chunks.clear();
+    pads.clear();
+  }
+
+  void drop_chunk(size_t i) {
+    cudaGraphExecDestroy(chunks[i].exec);
+    chunks.erase(chunks.begin() + long(i));
+  }
+
+  // padded pair of `stream` with `elems` doubles each (LRU, at most kMaxPads pairs)
+  int get_pads(cudaStream_t stream, size_t elems, double** out) {
+    for (auto& ps : pads)
+      if (ps.stream == stream && ps.elems == elems) {
+        ps.used = ++tick;
+        out[0] = ps.pad[0];
+        out[1] = ps.pad[1];
+        return SK_OK;
+      }
+    for (size_t i = 0; i < pads.size();)  // a different size on this stream, or the LRU pair when full
+      if (pads[i].stream == stream || (pads.size() >= kMaxPads && lru_pads() == i)) {
+        release_pads(i);
+        i = 0;
+      } else {
+        ++i;
+      }
+    ChPads ps;
+    ps.stream = stream;
+    ps.elems = elems;
+    for (double*& b : ps.pad) {
+      const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&b), elems * 8);
+      if (e != cudaSuccess) {
+        if (ps.pad[0]) cudaFree(ps.pad[0]);
+        return cuda_fail(e, "ghost-padded CH buffers");
+      }
+    }
+    ps.used = ++tick;
+    out[0] = ps.pad[0];
+    out[1] = ps.pad[1];
+    pads.push_back(ps);
+    return SK_OK;
+  }
+
+  size_t lru_pads() const {
+    size_t j = 0;
+    for (size_t i = 1; i < pads.size(); ++i)
+      if (pads[i].used < pads[j].used) j = i;
+    return j;
+  }
+
+  // free a padded pair and every graph that uses it (after the device drains)
+  void release_pads(size_t i) {
+    cudaDeviceSynchronize();
+    const ChPads ps = pads[i];
+    for (size_t k = 0; k < chunks.size();)
+      if (chunks[k].key.padded && chunks[k].key.stream == ps.stream) drop_chunk(k);
+      else ++k;
+    cudaFree(ps.pad[0]);
+    cudaFree(ps.pad[1]);
+    pads.erase(pads.begin() + long(i));
+  }
+};
+
+ChCache& ch_cache() {
+  static ChCache* c = new ChCache;  // never destroyed: graphs may outlive static destruction order
+  return *c;
 }
 
 }  // namespace sk
@@ -332,6 +368,8 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
   if (int st = check_width(bilap, g)) return st;
   if (!(dt > 0)) return fail(SK_ERR_INVALID_ARGUMENT, "dt must be positive");
   if (nsteps < 0) return fail(SK_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
+  if (p->formulation != SK_CH_FACTORED && p->formulation != SK_CH_COMPOSED)
+    return fail(SK_ERR_INVALID_ARGUMENT, "formulation must be SK_CH_FACTORED or SK_CH_COMPOSED");
   if (!c || !scratch || c == scratch) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
   if (result_is_scratch) *result_is_scratch = int(nsteps % 2);
   if (nsteps == 0 || g.rows == 0) return SK_OK;
@@ -366,66 +404,63 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
     return st;
   }
 
-  // fast path: whole chunks of kGraphSteps fused steps replayed as one graph
-  const int64_t full = (nsteps / kGraphSteps) * kGraphSteps;
-  if (full > 0) {
-    std::lock_guard<std::mutex> lock(g_ch_graph.mu);
-    // 3D factored: c -> pad -> ... -> pad -> c (TMA boxes, no wrap) unless SK_CH_PADDED=0
-    const char* env_pad = getenv("SK_CH_PADDED");
-    const bool padded = g.dim == 3 && p->formulation != SK_CH_COMPOSED && ptr_ok && chf3d_padded_ok(g) &&
-                        !(env_pad && env_pad[0] == '0');
-    const bool two = padded && chf3d2_ok(g) && p->formulation == SK_CH_FACTORED;
-    const double key_val[17] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
-                                double(g.n[0]), double(g.n[1]), double(g.n[2]),
-                                double(g.dim) + 10.0 * double(p->formulation),
-                                lap->orbit_coeff[0], lap->orbit_coeff[1], bilap->orbit_coeff[0],
-                                bilap->orbit_coeff[1], bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3],
-                                double(padded) + 2.0 * double(two)};
-    const void* key_ptr[4] = {c, scratch, lap, bilap};
-    bool hit = g_ch_graph.exec != nullptr;
-    for (int i = 0; i < 4 && hit; ++i) hit = key_ptr[i] == g_ch_graph.key_ptr[i];
-    for (int i = 0; i < 17 && hit; ++i) hit = key_val[i] == g_ch_graph.key_val[i];
+  // fast path: one step launched directly; longer runs as cached chunk graphs
+  if (nsteps == 1) return ch_step_fast(lap, bilap, g, p, dt, c, scratch, stream, ptr_ok);
+  const bool padded = g.dim == 3 && p->formulation == SK_CH_FACTORED && ptr_ok && chf3d_padded_ok(g) &&
+                      option(SK_OPT_CH_PADDED);
+  ChKey base;
+  const double v[16] = {dt, p->kappa, p->mobility, p->rho_w, p->c_alpha, p->c_beta, g.h,
+                        double(g.n[0]), double(g.n[1]), double(g.n[2]), double(g.dim) + 10.0 * double(p->formulation),
+                        lap->orbit_coeff[0], lap->orbit_coeff[1], bilap->orbit_coeff[0], bilap->orbit_coeff[1],
+                        bilap->orbit_coeff[2] + 7.0 * bilap->orbit_coeff[3]};
+  for (int i = 0; i < 16; ++i) base.v[i] = v[i];
+  base.lap_uid = lap->uid;
+  base.bilap_uid = bilap->uid;
+  base.epoch = option_epoch();
+  base.c = c;
+  base.scratch = scratch;
+  base.stream = stream;
+  base.padded = padded ? 1 : 0;
+  ChCache& cache = ch_cache();
+  std::lock_guard<std::mutex> lock(cache.mu);
+  for (int64_t done = 0; done < nsteps;) {
+    const int64_t rem = nsteps - done;
+    const int64_t len = rem <= kGraphSteps + 1 ? rem : kGraphSteps;  // never a 1-step chunk
+    ChKey key = base;
+    key.len = len;
+    key.to_scratch = (done + len == nsteps) && (nsteps % 2) ? 1 : 0;  // padded chunks: where Last writes
+    ChChunk* hit = nullptr;
+    for (auto& ch : cache.chunks)
+      if (ch.key == key) hit = &ch;
     if (!hit) {
-      if (g_ch_graph.exec) {
-        cudaGraphExecDestroy(g_ch_graph.exec);
-        g_ch_graph.exec = nullptr;
-      }
+      double* pad[2] = {nullptr, nullptr};
       if (padded) {
         const size_t elems = size_t(g.n[0] + 2 * kPadL) * size_t(g.n[1] + 2 * kPadT) * size_t(g.n[2]);
-        if (g_ch_graph.pad_elems != elems) {
-          for (double*& b : g_ch_graph.pad) {
-            if (b) cudaFree(b);
-            b = nullptr;
-          }
-          g_ch_graph.pad_elems = 0;
-          for (double*& b : g_ch_graph.pad) SK_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&b), elems * 8));
-          g_ch_graph.pad_elems = elems;
-        }
+        if (int st = cache.get_pads(stream, elems, pad)) return st;
       }
-      double* const* pad = g_ch_graph.pad;
+      if (cache.chunks.size() >= ChCache::kMaxChunks) {  // evict the least recently used graph
+        size_t j = 0;
+        for (size_t i = 1; i < cache.chunks.size(); ++i)
+          if (cache.chunks[i].used < cache.chunks[j].used) j = i;
+        cache.drop_chunk(j);
+      }
       cudaStream_t cap = stream ? stream : capture_stream();
       SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       int st = SK_OK;
       const int64_t l0 = g_launches.load();
-      // 3D padded chunks: single step into the padded field, 2-step launches
-      // (sk_chf3d2.cuh) pad -> pad, single step back into c (kGraphSteps even)
-      if (two) {
-        st = ch_step_fast(lap, bilap, g, p, dt, c, pad[0], cap, ptr_ok, kIoFirst, false, CfgChf3D2::H);
-        int cur = 0;
-        for (int k = 1; k + 1 < kGraphSteps && st == SK_OK; k += 2, cur ^= 1)
-          st = ch_two_steps_padded(lap, g, p, dt, pad[cur], pad[cur ^ 1], 1, cap);
-        if (st == SK_OK) st = ch_step_fast(lap, bilap, g, p, dt, pad[cur], c, cap, ptr_ok, kIoLast);
-      }
-      for (int k = 0; k < kGraphSteps && st == SK_OK && !two; ++k) {
-        if (!padded)
+      double* out_last = key.to_scratch ? scratch : c;
+      for (int64_t k = 0; k < len && st == SK_OK; ++k) {
+        if (!padded)  // plain ping-pong from c
           st = ch_step_fast(lap, bilap, g, p, dt, (k % 2) ? scratch : c, (k % 2) ? c : scratch, cap, ptr_ok);
         else if (k == 0)
           st = ch_step_fast(lap, bilap, g, p, dt, c, pad[0], cap, ptr_ok, kIoFirst);
-        else if (k + 1 < kGraphSteps)
+        else if (k + 1 < len)
           st = ch_step_fast(lap, bilap, g, p, dt, pad[(k - 1) % 2], pad[k % 2], cap, ptr_ok, kIoMid);
         else
-          st = ch_step_fast(lap, bilap, g, p, dt, pad[(k - 1) % 2], c, cap, ptr_ok, kIoLast);
+          st = ch_step_fast(lap, bilap, g, p, dt, pad[(k - 1) % 2], out_last, cap, ptr_ok, kIoLast);
       }
+      const int64_t launches = g_launches.load() - l0;
+      g_launches -= launches;  // capture does not execute; counted per replay below
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaStreamEndCapture(cap, &graph);
       if (st != SK_OK) {
@@ -433,24 +468,19 @@ int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid
         return st;
       }
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-      e = cudaGraphInstantiate(&g_ch_graph.exec, graph, 0);
+      ChChunk ch;
+      ch.key = key;
+      ch.launches = launches;
+      e = cudaGraphInstantiate(&ch.exec, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-      for (int i = 0; i < 4; ++i) g_ch_graph.key_ptr[i] = key_ptr[i];
-      for (int i = 0; i < 17; ++i) g_ch_graph.key_val[i] = key_val[i];
-      g_ch_graph.launches = g_launches.load() - l0;
-      g_launches -= g_ch_graph.launches;  // capture does not execute; counted per replay below
+      cache.chunks.push_back(ch);
+      hit = &cache.chunks.back();
     }
-    for (int64_t k = 0; k < full; k += kGraphSteps) {
-      SK_CUDA_TRY(cudaGraphLaunch(g_ch_graph.exec, stream));
-      g_launches += g_ch_graph.launches;
-    }
-  }
-  for (int64_t k = full; k < nsteps; ++k) {
-    // kGraphSteps is even, so after `full` steps the field is back in c
-    const bool from_c = (k % 2) == 0;
-    if (int st = ch_step_fast(lap, bilap, g, p, dt, from_c ? c : scratch, from_c ? scratch : c, stream, ptr_ok))
-      return st;
+    hit->used = ++cache.tick;
+    SK_CUDA_TRY(cudaGraphLaunch(hit->exec, stream));
+    g_launches += hit->launches;
+    done += len;
   }
   return SK_OK;
 }
@@ -467,6 +497,8 @@ int sk_ch_explicit_slab(const sk_stencil* lap, const sk_stencil* bilap, const sk
     return fail(SK_ERR_INVALID_ARGUMENT, "slab stepping needs the 7-point L and its 25-point composition");
   if (g.n[0] < 5 || g.n[1] < 5) return fail(SK_ERR_STENCIL_WIDER_THAN_GRID, "periodic axis narrower than stencil support");
   if (!(dt > 0)) return fail(SK_ERR_INVALID_ARGUMENT, "dt must be positive");
+  if (p->formulation != SK_CH_FACTORED && p->formulation != SK_CH_COMPOSED)
+    return fail(SK_ERR_INVALID_ARGUMENT, "formulation must be SK_CH_FACTORED or SK_CH_COMPOSED");
   if (!in_ghosted || !out) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
   const int64_t plane = g.n[0] * g.n[1];
   const double* in = in_ghosted + 2 * plane;  // first interior plane
@@ -479,18 +511,34 @@ int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk
   GridInfo g;
   if (int st = grid_info(gd, &g)) return st;
   if (!c_host && g.rows > 0) return fail(SK_ERR_INVALID_ARGUMENT, "null host field");
-  // c_host -> c (device), steps ping-pong c <-> s, result -> c_host
+  if (nsteps < 0) return fail(SK_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
+  if (g.rows == 0) return SK_OK;
+  // c_host -> c (device), steps ping-pong c <-> s, result -> c_host. The
+  // device pair is per host thread and kept between calls, so repeated calls
+  // replay the cached chunk graphs (keyed by the buffers) instead of
+  // re-capturing them.
+  struct Staging {
+    double* buf = nullptr;
+    size_t elems = 0;
+  };
+  thread_local Staging stage;
   cudaStream_t hs = host_stream();
-  AsyncBuf s(hs);
-  SK_CUDA_TRY(s.alloc(sizeof(double) * size_t(g.rows)));
-  return host_roundtrip(c_host, size_t(g.rows), nullptr, 0, [&](const double* c, double*, cudaStream_t st) {
-    int in_scratch = 0;
-    double* cd = const_cast<double*>(c);
-    if (int e = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, cd, s.d(), &in_scratch, st)) return e;
-    SK_CUDA_TRY(cudaMemcpyAsync(c_host, in_scratch ? s.d() : cd, sizeof(double) * size_t(g.rows),
-                                cudaMemcpyDeviceToHost, st));
-    return int(SK_OK);
-  });
+  const size_t n = size_t(g.rows);
+  if (stage.elems < n) {
+    if (stage.buf) SK_CUDA_TRY(cudaFree(stage.buf));
+    stage.buf = nullptr;
+    stage.elems = 0;
+    SK_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&stage.buf), 2 * n * sizeof(double)));
+    stage.elems = n;
+  }
+  double* cd = stage.buf;
+  double* sd = stage.buf + stage.elems;
+  SK_CUDA_TRY(cudaMemcpyAsync(cd, c_host, n * sizeof(double), cudaMemcpyHostToDevice, hs));
+  int in_scratch = 0;
+  if (int e = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, cd, sd, &in_scratch, hs)) return e;
+  SK_CUDA_TRY(cudaMemcpyAsync(c_host, in_scratch ? sd : cd, n * sizeof(double), cudaMemcpyDeviceToHost, hs));
+  SK_CUDA_TRY(cudaStreamSynchronize(hs));
+  return SK_OK;
 }
 
 int sk_free_energy(const sk_grid_desc* gd, const sk_ch_params* p, const double* c, double* energy, void* stream_p) {

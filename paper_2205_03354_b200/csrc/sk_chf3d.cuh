@@ -42,11 +42,11 @@ namespace sk {
 // Ghost-padded field of the TMA path: row pitch nx + 2 kPadL, kPadT ghost
 // rows above and below; interior x at column x + kPadL (128 B-aligned rows
 // and tiles, so the interior stores are whole lines), ghosts x = -2, -1 and
-// nx, nx + 1 at columns kPadL - 2 .. and kPadL + nx ... (images: 4 columns, 4 rows)
+// nx, nx + 1 at columns kPadL - 2 .. and kPadL + nx ... (images: 4 columns, 2 rows)
 #ifndef SK_PADL
 #define SK_PADL 16
 #endif
-constexpr int kPadL = SK_PADL, kPadT = 4;  // 4 ghost rows: the 2-step kernel's boxes (sk_chf3d2.cuh)
+constexpr int kPadL = SK_PADL, kPadT = 2;  // ghost rows above and below (the radius-2 periodic images)
 // L2 policy of the TMA loads: evict_last keeps tile halos for the
 // y-neighbour tile's CTA (measured +0.5%; evict_first: -19%)
 #ifndef SK_TMA_HINT
@@ -214,14 +214,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
     double* outp = a.v + int64_t(sg.z0) * opp + (gy0 + (OUT ? kPadT : 0)) * opx + gx0 + (OUT ? kPadL : 0);
     // OUT 1: periodic images in the ghost frame: columns 0..3 and nx-4..nx-1
     // (whole 32 B sectors: no partial-sector writes), rows 0..g-1 and ny-g..ny-1
-    // (g = a.ghost: 2, or 4 when a 2-step launch reads the field)
+    // (g = a.ghost = 2)
     const int64_t gdx_ = OUT ? (gx0 < 4 ? a.nx : (gx0 >= a.nx - 4 ? -a.nx : 0)) : 0;
     const int64_t gdy_ = OUT ? (gy0 < a.ghost ? a.ny : (gy0 >= a.ny - a.ghost ? -a.ny : 0)) * opx : 0;
-#ifdef SK_NO_GHOST  // timing experiment only (wrong results)
-    const int64_t gdx = 0 * gdx_, gdy = 0 * gdy_;
-#else
     const int64_t gdx = gdx_, gdy = gdy_;
-#endif
     const int np = sg.len + 2 * R;
 
     // one step: plane k landed; DO_MU: mu of plane k-1; DO_OUT: output plane k-2

@@ -16,6 +16,16 @@ thread_local std::string t_err;
 
 std::atomic<int64_t> g_launches{0};
 
+namespace {
+// sk_set_option values (include/sk_cuda.h enum sk_option order); defaults
+// are the measured-fastest paths
+std::atomic<int> g_options[SK_OPT_COUNT] = {1, 1, 1, 1, -1, 1, 1, 0};
+std::atomic<uint64_t> g_option_epoch{0};
+}  // namespace
+
+int option(int id) { return g_options[id].load(std::memory_order_relaxed); }
+uint64_t option_epoch() { return g_option_epoch.load(std::memory_order_relaxed); }
+
 void set_error(int status, const std::string& msg) {
   t_err = std::string(sk_status_name(status)) + ": " + msg;
 }
@@ -104,7 +114,22 @@ const char* sk_status_name(int s) {
   return "UnknownError";
 }
 
-int sk_version(void) { return 1; }
+int sk_version(void) { return 2; }
+
+int sk_set_option(int opt, int value) {
+  if (opt < 0 || opt >= SK_OPT_COUNT) return fail(SK_ERR_INVALID_ARGUMENT, "unknown option");
+  const int lo = opt == SK_OPT_CG_COOP ? -1 : 0;
+  if (value < lo || value > 1) return fail(SK_ERR_INVALID_ARGUMENT, "option value out of range");
+  if (g_options[opt].exchange(value) != value) g_option_epoch.fetch_add(1);
+  return SK_OK;
+}
+
+int sk_get_option(int opt, int* value) {
+  if (opt < 0 || opt >= SK_OPT_COUNT) return fail(SK_ERR_INVALID_ARGUMENT, "unknown option");
+  if (!value) return fail(SK_ERR_INVALID_ARGUMENT, "null output pointer");
+  *value = g_options[opt].load();
+  return SK_OK;
+}
 
 int64_t sk_launch_count(void) { return g_launches.load(); }
 
@@ -150,6 +175,19 @@ int sk_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
 
 int sk_stream_sync(void* stream) {
   SK_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  return SK_OK;
+}
+
+int sk_stream_create(void** out) {
+  if (!out) return fail(SK_ERR_INVALID_ARGUMENT, "null output pointer");
+  cudaStream_t s = nullptr;
+  SK_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
+  return SK_OK;
+}
+
+int sk_stream_destroy(void* stream) {
+  if (stream) SK_CUDA_TRY(cudaStreamDestroy(as_stream(stream)));
   return SK_OK;
 }
 

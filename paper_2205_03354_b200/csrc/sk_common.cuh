@@ -18,6 +18,10 @@ void set_error(int status, const std::string& msg);
 int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 extern std::atomic<int64_t> g_launches;
+// sk_set_option state: current value, and a counter bumped on every change
+// (cached graphs / plans record it and rebuild when it moves)
+int option(int id);
+uint64_t option_epoch();
 
 #define SK_CUDA_TRY(expr)                                        \
   do {                                                           \

@@ -311,12 +311,11 @@ int sk_ch_imex_create(const sk_grid_desc* gd, const sk_ch_params* p, const sk_so
   if (st == SK_OK) st = csr_build_sell(s->B, hs);
   // matrix-free implicit operator on the kernels' symmetric radius-2 classes
   // (grid at least the stencil width: no wrapped duplicates) unless
-  // SK_IMEX_MATRIX_FREE=0 (CSR SpMV, bit-identical products)
+  // SK_OPT_IMEX_MATRIX_FREE = 0 (CSR SpMV, bit-identical products)
   if (st == SK_OK) {
-    const char* env = getenv("SK_IMEX_MATRIX_FREE");
     bool wide = true;
     for (int a = 0; a < g.dim; ++a) wide &= g.n[a] >= 5;
-    s->matrix_free = wide && (s->bilap->kclass == 1 || s->bilap->kclass == 2) && !(env && env[0] == '0');
+    s->matrix_free = wide && (s->bilap->kclass == 1 || s->bilap->kclass == 2) && option(SK_OPT_IMEX_MATRIX_FREE);
   }
   if (st == SK_OK && cudaStreamSynchronize(hs) != cudaSuccess) st = fail(SK_ERR_CUDA, "IMEX setup");
   if (st != SK_OK) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "sk_common.cuh"
@@ -25,11 +26,25 @@ struct sk_stencil {
   double orbit_coeff[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int* d_off = nullptr;       // device copy for the generic kernel / assembly
   double* d_coeff = nullptr;
-  // cached CUDA graph of sk_composed_apply_repeat
+  // cached CUDA graph of sk_composed_apply_repeat: the captured kernels bake
+  // in the buffers, the grid (extents, boundary kinds, h -> weights) and the
+  // option epoch, all part of the key; rep_mu serialises concurrent callers
+  struct RepKey {
+    const void* ptr[3] = {nullptr, nullptr, nullptr};
+    int repeats = 0, dim = 0;
+    int64_t n[3] = {0, 0, 0};
+    int bc[3] = {0, 0, 0};
+    double h = 0;
+    uint64_t epoch = 0;
+    bool operator==(const RepKey& o) const {
+      return ptr[0] == o.ptr[0] && ptr[1] == o.ptr[1] && ptr[2] == o.ptr[2] && repeats == o.repeats &&
+             dim == o.dim && n[0] == o.n[0] && n[1] == o.n[1] && n[2] == o.n[2] && bc[0] == o.bc[0] &&
+             bc[1] == o.bc[1] && bc[2] == o.bc[2] && h == o.h && epoch == o.epoch;
+    }
+  };
+  std::mutex rep_mu;
   cudaGraphExec_t rep_exec = nullptr;
-  const void* rep_key[4] = {nullptr, nullptr, nullptr, nullptr};
-  int64_t rep_n[3] = {0, 0, 0};
-  int rep_repeats = 0;
+  RepKey rep_key;
   ~sk_stencil();
 };
 

@@ -164,10 +164,9 @@ int launch_2d(const Apply2DArgs& a, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const char* env = getenv("SK_PDL");
   // (the fused CG apply follows K2 of the previous iteration: measured slower
   // with the programmatic edge)
-  if ((env && env[0] == '0') || M == Mode::CgApply) cfg.numAttrs = 0;
+  if (!option(SK_OPT_PDL) || M == Mode::CgApply) cfg.numAttrs = 0;
   SK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
   SK_LAUNCH_CHECK("stencil2d_kernel");
   return SK_OK;
@@ -183,10 +182,9 @@ int launch_3d(Args3D a, cudaStream_t stream) {
   static int once = set_smem(bulk, bulk_smem) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, C::SMEM_BYTES);
   if (once != SK_OK) return once;
   // rotated columns (seg_of: balanced ranges, neighbour tiles in phase);
-  // SK_ZROT=0: lockstep for the radius-2 apply (halo rows from L2), balanced
-  // for the issue-bound radius-4 apply and the composed CH step
-  const char* zr = getenv("SK_ZROT");
-  a.zrot = (!a.z_ghosted && !(zr && zr[0] == '0')) ? 1 : 0;
+  // z-ghosted slabs: lockstep for the radius-2 apply (halo rows from L2),
+  // balanced otherwise
+  a.zrot = a.z_ghosted ? 0 : 1;
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/!a.zrot && C::R == 2 && M == Mode::Apply);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   if (a.bulk_ok)  // (after persistent_grid, which may clear it)
@@ -293,8 +291,7 @@ static int launch_fac73(Args3D a, double h_m2, cudaStream_t stream) {
   auto fallback = fac73_kernel<C, true>;
   static int once = set_smem(bulk, SM::BYTES) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, SM::BYTES_FB);
   if (once != SK_OK) return once;
-  const char* zr = getenv("SK_ZROT");
-  a.zrot = !(zr && zr[0] == '0') ? 1 : 0;
+  a.zrot = 1;
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   if (a.bulk_ok)
@@ -341,9 +338,7 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
                 aligned16(u) && aligned16(v);
     if (per && is_l4l4(s)) {  // B = compose(L4, L4) on a periodic grid: two fused L4 passes possible
-      // opt-in (SK_F73=1): measured slower than the literal kernel (sk_fac3d.cuh, Status)
-      const char* e = getenv("SK_F73");
-      if (e && e[0] == '1') return launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
+      if (option(SK_OPT_APPLY73_FACTORED)) return launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
     }
     if (a.bulk_ok && a.nx >= Cfg3R4P::TX + 2 * Cfg3R4P::R && a.ny >= Cfg3R4P::TY + 2 * Cfg3R4P::R)
       return launch_3d<Mode::Apply, Cfg3R4P>(a, stream);
@@ -354,12 +349,11 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
 
 // Matrix-free CG: q = A p fused with p.q -> alpha (stream3d_kernel<..., PQ>)
 // for the 3D streaming stencils; kApplyPqUnsupported: the caller runs the
-// apply and a separate p.q pass. SK_CG_PQ=0 disables it.
+// apply and a separate p.q pass. SK_OPT_CG_PQ = 0 disables it.
 bool apply_pq_supported(const sk_stencil* s, const GridInfo& g) {
-  const char* env = getenv("SK_CG_PQ");
   // radius 2 only: the radius-4 kernel (234+ registers) slows down with the
   // epilogue (config 5 matrix-free: 0.457 -> 0.494 ms per iteration)
-  return !(env && env[0] == '0') && g.dim == 3 && s->kclass == 2 && streamable(s, g, 2);
+  return option(SK_OPT_CG_PQ) && g.dim == 3 && s->kclass == 2 && streamable(s, g, 2);
 }
 
 int launch_apply_pq(const sk_stencil* s, const GridInfo& g, const double* p, double* q, CgState* st,
@@ -464,12 +458,20 @@ int sk_composed_apply_repeat(const sk_stencil* s_c, const sk_grid_desc* gd, cons
   if (repeats == 0 || g.rows == 0) return SK_OK;
   if (!u || !v0 || !v1 || u == v0 || u == v1) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
   cudaStream_t stream = as_stream(stream_p);
-  const bool hit = s->rep_exec && s->rep_key[0] == u && s->rep_key[1] == v0 && s->rep_key[2] == v1 &&
-                   s->rep_repeats == repeats && s->rep_n[0] == g.n[0] && s->rep_n[1] == g.n[1] &&
-                   s->rep_n[2] == g.n[2] && s->rep_key[3] == reinterpret_cast<const void*>(
-                                                               static_cast<uintptr_t>(gd->bc[0] | gd->bc[1] << 2 |
-                                                                                      gd->bc[2] << 4 | 1 << 8));
-  if (!hit) {
+  sk_stencil::RepKey key;
+  key.ptr[0] = u;
+  key.ptr[1] = v0;
+  key.ptr[2] = v1;
+  key.repeats = repeats;
+  key.dim = g.dim;
+  for (int a = 0; a < 3; ++a) {
+    key.n[a] = g.n[a];
+    key.bc[a] = g.bc[a];
+  }
+  key.h = g.h;
+  key.epoch = option_epoch();
+  std::lock_guard<std::mutex> lock(s->rep_mu);
+  if (!(s->rep_exec && s->rep_key == key)) {
     if (s->rep_exec) {
       cudaGraphExecDestroy(s->rep_exec);
       s->rep_exec = nullptr;
@@ -477,8 +479,10 @@ int sk_composed_apply_repeat(const sk_stencil* s_c, const sk_grid_desc* gd, cons
     cudaStream_t cap = stream ? stream : capture_stream();
     SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     int st = SK_OK;
+    const int64_t l0 = g_launches.load();
     for (int r = 0; r < repeats && st == SK_OK; ++r)
       st = launch_apply(s, g, u, (r % 2) ? v1 : v0, cap, /*input_stable=*/true);
+    g_launches -= g_launches.load() - l0;  // capture does not execute; counted per replay below
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap, &graph);
     if (st != SK_OK) {
@@ -489,16 +493,9 @@ int sk_composed_apply_repeat(const sk_stencil* s_c, const sk_grid_desc* gd, cons
     e = cudaGraphInstantiate(&s->rep_exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-    s->rep_key[0] = u;
-    s->rep_key[1] = v0;
-    s->rep_key[2] = v1;
-    s->rep_key[3] = reinterpret_cast<const void*>(
-        static_cast<uintptr_t>(gd->bc[0] | gd->bc[1] << 2 | gd->bc[2] << 4 | 1 << 8));
-    s->rep_repeats = repeats;
-    for (int a = 0; a < 3; ++a) s->rep_n[a] = g.n[a];
-  } else {
-    g_launches.fetch_add(repeats);  // the graph replays `repeats` kernels
+    s->rep_key = key;
   }
+  g_launches.fetch_add(repeats);  // the graph replays `repeats` kernels
   SK_CUDA_TRY(cudaGraphLaunch(s->rep_exec, stream));
   return SK_OK;
 }

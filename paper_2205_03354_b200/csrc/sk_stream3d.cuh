@@ -77,7 +77,7 @@ struct Args3D {
   CgState* cg;       // PQ kernels (matrix-free CG, sk_cg.cu): q = A p fused with p.q -> alpha
   double* cg_partials;
   int zchunk;        // unit order (z-chunk, tile [y fastest], z): concurrent CTAs stay close in z
-  int ghost;         // chf3d OUT 1: ghost rows written on each side (2; 4 when a 2-step launch reads them)
+  int ghost;         // chf3d OUT 1: ghost rows written on each side (2)
   int zrot;          // periodic z, zchunk = nz: every tile column is rotated so CTA range starts sit at
                      // the same planes in every column (seg_of): neighbour tiles are streamed in phase
 };
@@ -96,8 +96,6 @@ inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
   if (units >= (int64_t(1) << 31) || a.nz >= (int64_t(1) << 31)) return 0;
   const int64_t slots = int64_t(num_sms) * C::MIN_BLOCKS;
   int64_t grid = slots < units ? slots : units;
-  const char* sched = getenv("SK_SCHED");  // experiments: "balanced" / "lockstep" override
-  if (sched) lockstep = sched[0] == 'l';
   if (lockstep) {
     // lockstep: one CTA per (tile, z-chunk) with the most z-chunks
     // that still fit one wave; every CTA starts at a chunk top, so the tiles
@@ -121,10 +119,6 @@ inline int64_t persistent_grid(Args3D& a, int num_sms, bool lockstep) {
       a.zchunk = int(d);
       break;
     }
-  if (const char* zc = getenv("SK_ZCHUNK")) {  // experiments
-    const int64_t v = atoll(zc);
-    if (v >= 1 && a.nz % v == 0) a.zchunk = int(v);
-  }
   return grid;
 }
 

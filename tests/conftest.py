@@ -33,3 +33,20 @@ def lib():
     from paper_2205_03354_b200 import _lib
 
     return _lib.ensure_device(0)
+
+
+@pytest.fixture
+def sk_option():
+    """Set library execution options (sk_set_option) for one test; every changed
+    option is restored afterwards."""
+    from paper_2205_03354_b200 import _lib
+
+    saved = {}
+
+    def setter(name, value):
+        old = _lib.set_option(name, value)
+        saved.setdefault(name, old)
+
+    yield setter
+    for name, value in saved.items():
+        _lib.set_option(name, value)

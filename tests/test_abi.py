@@ -78,3 +78,30 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.ChParams) == 5 * 8 + 8
     assert C.sizeof(_lib.SolveOptionsC) == 8 + 8 + 4 + 4 + 4 + 4
     assert C.sizeof(_lib.SolveReportC) == 32
+
+
+def test_options_are_explicit_and_validated():
+    # execution options are set through sk_set_option only (host-side, no GPU needed)
+    lib = _lib.load()
+    v = C.c_int()
+    for name, opt in _lib.OPTIONS.items():
+        assert lib.sk_get_option(opt, C.byref(v)) == 0
+    assert lib.sk_set_option(99, 1) == Errc.invalid_argument + 1
+    assert lib.sk_set_option(_lib.OPTIONS["ch_padded"], 7) == Errc.invalid_argument + 1
+    with _lib.options(ch_padded=0, cg_coop=1):
+        lib.sk_get_option(_lib.OPTIONS["ch_padded"], C.byref(v))
+        assert v.value == 0
+    lib.sk_get_option(_lib.OPTIONS["ch_padded"], C.byref(v))
+    assert v.value == 1
+
+
+def test_product_never_reads_the_environment():
+    # a stray environment variable must not change which kernel runs
+    csrc = ROOT / "paper_2205_03354_b200" / "csrc"
+    for f in list(csrc.glob("*.cu")) + list(csrc.glob("*.cuh")) + list(csrc.glob("*.hpp")):
+        assert "getenv" not in f.read_text(), f.name
+    for f in (ROOT / "paper_2205_03354_b200").glob("*.py"):
+        if f.name == "build_ext.py":  # the build tool may locate nvcc through $NVCC
+            continue
+        text = f.read_text()
+        assert "os.environ" not in text and "getenv" not in text, f.name

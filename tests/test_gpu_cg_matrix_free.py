@@ -55,7 +55,7 @@ def test_matrix_free_and_csr_cg_agree_config2():
 
 @pytest.mark.parametrize("bc", [BoundaryKind.clamped, BoundaryKind.simply_supported, BoundaryKind.periodic])
 @pytest.mark.parametrize("check_every", [0, 7])
-def test_fused_2d_iterations_match_unfused(monkeypatch, bc, check_every):
+def test_fused_2d_iterations_match_unfused(sk_option, bc, check_every):
     # the two-kernel 2D iteration (p' = r + beta p on the tile load, p.q in
     # the apply's epilogue) follows the four-kernel one: same recurrence, only
     # the p.q summation order differs. Odd check_every exercises the p / p2
@@ -67,13 +67,13 @@ def test_fused_2d_iterations_match_unfused(monkeypatch, bc, check_every):
     b -= b.mean() if bc == BoundaryKind.periodic else 0.0
     o = SolveOptions(rel_tol=1e-9, check_every=check_every, deflate_mean=bc == BoundaryKind.periodic)
     if check_every:
-        monkeypatch.setenv("SK_CG_DEVICE_LOOP", "0")  # the unrolled-graph fallback
+        sk_option("cg_device_loop", 0)  # the unrolled-graph fallback
     reps = []
     xs = []
     # cooperative kernel (forced), two-kernel graph, four-kernel graph
-    for fused, coop in (("1", "1"), ("1", "0"), ("0", "0")):
-        monkeypatch.setenv("SK_CG_FUSED", fused)
-        monkeypatch.setenv("SK_CG_COOP", coop)
+    for fused, coop in ((1, 1), (1, 0), (0, 0)):
+        sk_option("cg_fused", fused)
+        sk_option("cg_coop", coop)
         rep = SolveReport()
         xs.append(cg_solve_stencil(DeviceStencil(bilaplacian(2)), g, b, o, rep))  # new stencil -> new plan
         reps.append(rep)
@@ -87,7 +87,7 @@ def test_fused_2d_iterations_match_unfused(monkeypatch, bc, check_every):
 
 @pytest.mark.parametrize("bc", [BoundaryKind.clamped, BoundaryKind.simply_supported, BoundaryKind.periodic])
 @pytest.mark.parametrize("check_every", [0, 7])
-def test_3d_apply_pq_matches_separate_pass(monkeypatch, bc, check_every):
+def test_3d_apply_pq_matches_separate_pass(sk_option, bc, check_every):
     # 3D radius-2 stencils: p.q reduced in the streaming apply's epilogue
     # (three kernels per iteration) follows the separate p.q pass: same
     # recurrence, only the p.q summation order differs
@@ -97,10 +97,10 @@ def test_3d_apply_pq_matches_separate_pass(monkeypatch, bc, check_every):
     b -= b.mean() if bc == BoundaryKind.periodic else 0.0
     o = SolveOptions(rel_tol=1e-9, check_every=check_every, deflate_mean=bc == BoundaryKind.periodic)
     if check_every:
-        monkeypatch.setenv("SK_CG_DEVICE_LOOP", "0")
+        sk_option("cg_device_loop", 0)
     reps, xs = [], []
-    for pq in ("1", "0"):
-        monkeypatch.setenv("SK_CG_PQ", pq)
+    for pq in (1, 0):
+        sk_option("cg_pq", pq)
         rep = SolveReport()
         xs.append(cg_solve_stencil(DeviceStencil(bilaplacian(3)), g, b, o, rep))
         reps.append(rep)

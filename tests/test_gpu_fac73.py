@@ -22,7 +22,7 @@ def rel_max(a, b):
 
 @pytest.mark.parametrize("dims", [(64, 64, 64), (128, 96, 40), (72, 48, 9), (66, 34, 11), (130, 50, 20),
                                   (192, 160, 33)])
-def test_fac73_vs_literal_and_oracle(orc, dims, monkeypatch):
+def test_fac73_vs_literal_and_oracle(orc, dims, sk_option):
     # whole and partial tiles, z extents down to 9, odd widths (8-byte loader)
     h = 1.0 / max(dims)
     g = GridSpec(dim=3, n=list(dims), h=h, origin=[0.0] * 3, bc=[BoundaryKind.periodic] * 3)
@@ -31,7 +31,7 @@ def test_fac73_vs_literal_and_oracle(orc, dims, monkeypatch):
     u = rng.uniform(-1, 1, g.unknown_count())
     out = {}
     for flag in ("1", "0"):
-        monkeypatch.setenv("SK_F73", flag)
+        sk_option("apply73_factored", int(flag))
         out[flag] = composed_apply(s, g, u)
     ref = orc.apply_direct(s, g, u)
     assert rel_max(out["1"], ref) <= 1e-12
@@ -39,7 +39,7 @@ def test_fac73_vs_literal_and_oracle(orc, dims, monkeypatch):
     assert rel_max(out["1"], out["0"]) <= 1e-12
 
 
-def test_fac73_smooth_input(orc, monkeypatch):
+def test_fac73_smooth_input(orc, sk_option):
     # smooth field (large cancellation in B u): still within the bar
     n = 96
     h = 1.0 / n
@@ -48,12 +48,12 @@ def test_fac73_smooth_input(orc, monkeypatch):
     u = (np.sin(2 * np.pi * x)[None, None, :] * np.sin(2 * np.pi * x)[None, :, None] *
          np.cos(4 * np.pi * x)[:, None, None]).ravel() + 1e-3 * np.random.default_rng(1).uniform(-1, 1, n ** 3)
     s = bilaplacian(3, 4)
-    monkeypatch.setenv("SK_F73", "1")
+    sk_option("apply73_factored", 1)
     v = composed_apply(s, g, u)
     assert rel_max(v, orc.apply_direct(s, g, u)) <= 1e-12
 
 
-def test_fac73_not_used_off_periodic(orc, monkeypatch):
+def test_fac73_not_used_off_periodic(orc, sk_option):
     # clamped grids keep the literal kernel (the factorisation does not hold at
     # reflected boundaries): SK_F73 has no effect there
     g = GridSpec(dim=3, n=[41, 41, 41], h=1.0 / 40, origin=[0.0] * 3, bc=[BoundaryKind.clamped] * 3)
@@ -61,7 +61,7 @@ def test_fac73_not_used_off_periodic(orc, monkeypatch):
     u = np.random.default_rng(3).uniform(-1, 1, g.unknown_count())
     out = {}
     for flag in ("1", "0"):
-        monkeypatch.setenv("SK_F73", flag)
+        sk_option("apply73_factored", int(flag))
         out[flag] = composed_apply(s, g, u)
     assert np.array_equal(out["1"], out["0"])
     assert rel_max(out["1"], orc.apply_direct(s, g, u)) <= 1e-12

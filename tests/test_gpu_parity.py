@@ -165,7 +165,7 @@ def test_ch_graph_chunks_and_remainder(orc):
 
 
 @pytest.mark.parametrize("n,steps", [(64, 230), (128, 100)])
-def test_ch_3d_padded_path(orc, n, steps, monkeypatch):
+def test_ch_3d_padded_path(orc, n, steps, sk_option):
     # >= 100 steps of the 3D factored form run as graph chunks through ghost-padded
     # fields (TMA kernel); the result is bit-identical to the plain cp.async path
     # and matches the oracle
@@ -176,13 +176,84 @@ def test_ch_3d_padded_path(orc, n, steps, monkeypatch):
     c0 = 0.05 * uniform(4, g.unknown_count())
     out = {}
     for flag in ("1", "0"):
-        monkeypatch.setenv("SK_CH_PADDED", flag)
+        sk_option("ch_padded", int(flag))
         st = CahnHilliardState(g, c0.copy())
         CahnHilliardExplicit(g, p).step(st, dt, steps)
         out[flag] = st.c.copy()
     assert np.array_equal(out["1"], out["0"])
     ref = orc.ch_explicit(3, n, h, p, dt, steps, c0)
     assert np.linalg.norm(out["1"] - ref) / np.linalg.norm(ref) <= 1e-9
+
+
+@pytest.mark.parametrize("steps", [1, 2, 3, 20, 101, 102, 203])
+def test_ch_3d_chunking_any_step_count(orc, steps, sk_option):
+    # every step count >= 2 runs as chunk graphs (padded TMA path for the 3D
+    # factored form): bit-identical to the plain path, the result in the buffer
+    # the ping-pong parity names, and within the bar of the oracle
+    n = 64
+    p = CahnHilliardParams.from_epsilon(0.02)
+    h = 1.0 / n
+    dt = 0.2 * h ** 4 / (144 * p.kappa)
+    g = make_periodic_grid(3, n, h)
+    c0 = 0.05 * uniform(8, g.unknown_count())
+    out = {}
+    for flag in (1, 0):
+        sk_option("ch_padded", flag)
+        st = CahnHilliardExplicit(g, p)
+        c, s = DeviceArray.from_host(c0), DeviceArray(g.unknown_count())
+        res = st.run_device(c, s, dt, steps)
+        assert (res is s) == bool(steps % 2)
+        out[flag] = res.to_host()
+    assert np.array_equal(out[1], out[0])
+    ref = orc.ch_explicit(3, n, h, p, dt, steps, c0)
+    assert np.linalg.norm(out[1] - ref) / np.linalg.norm(ref) <= 1e-9
+
+
+def test_ch_3d_concurrent_streams(lib):
+    # two steppers of the same grid size on two streams, issued back to back
+    # without a sync: each stream has its own ghost-padded pair, so the runs
+    # cannot corrupt each other; results equal the sequential runs
+    import ctypes as C
+
+    n, steps = 64, 100
+    p = CahnHilliardParams.from_epsilon(0.02)
+    h = 1.0 / n
+    dt = 0.2 * h ** 4 / (144 * p.kappa)
+    g = make_periodic_grid(3, n, h)
+    fields = [0.05 * uniform(20 + k, g.unknown_count()) for k in range(2)]
+    seq = []
+    for f in fields:
+        st = CahnHilliardState(g, f.copy())
+        CahnHilliardExplicit(g, p).step(st, dt, steps)
+        seq.append(st.c)
+    streams = [C.c_void_p(), C.c_void_p()]
+    for s_ in streams:
+        assert lib.sk_stream_create(C.byref(s_)) == 0
+    try:
+        steppers = [CahnHilliardExplicit(g, p) for _ in fields]
+        bufs = [(DeviceArray.from_host(f), DeviceArray(g.unknown_count())) for f in fields]
+        for rep in range(3):  # replays of the cached graphs interleave too
+            for k in range(2):
+                bufs[k][0].upload(fields[k])
+            res = [steppers[k].run_device(bufs[k][0], bufs[k][1], dt, steps, streams[k]) for k in range(2)]
+            for s_ in streams:
+                assert lib.sk_stream_sync(s_) == 0
+            for k in range(2):
+                assert np.array_equal(res[k].to_host(), seq[k]), (rep, k)
+    finally:
+        for s_ in streams:
+            lib.sk_stream_destroy(s_)
+
+
+def test_ch_rejects_unknown_formulation():
+    g = make_periodic_grid(3, 32, 1.0 / 32)
+    p = CahnHilliardParams.from_epsilon(0.02)
+    st = CahnHilliardExplicit(g, p)
+    st._p.formulation = 2
+    c, s = DeviceArray(g.unknown_count()), DeviceArray(g.unknown_count())
+    with pytest.raises(StencilkitError) as e:
+        st.run_device(c, s, 1e-9, 3)
+    assert e.value.code == Errc.invalid_argument
 
 
 def test_ch_rejects_non_periodic():
@@ -348,7 +419,7 @@ def test_cg_biharmonic_clamped_vs_oracle(orc, dim, acc, intervals, tol):
 
 @pytest.mark.parametrize("dims,steps", [((64, 32, 5), 100), ((128, 64, 6), 230), ((96, 40, 7), 120), ((64, 32, 9), 100),
                                         ((128, 48), 150), ((67, 36, 9), 60), ((130, 34, 8), 40)])
-def test_ch_noncubic_grids(orc, dims, steps, monkeypatch):
+def test_ch_noncubic_grids(orc, dims, steps, sk_option):
     # non-cubic periodic grids, tiny z extents (z wrap inside one chunk), the
     # ghost-padded TMA path (whole tiles) and the plain path, vs the oracle
     from paper_2205_03354_b200.grid import GridSpec
@@ -361,7 +432,7 @@ def test_ch_noncubic_grids(orc, dims, steps, monkeypatch):
     c0 = 0.05 * uniform(6, g.unknown_count())
     out = {}
     for flag in ("1", "0"):
-        monkeypatch.setenv("SK_CH_PADDED", flag)
+        sk_option("ch_padded", int(flag))
         st = CahnHilliardState(g, c0.copy())
         CahnHilliardExplicit(g, p).step(st, dt, steps)
         out[flag] = st.c.copy()

@@ -30,8 +30,8 @@ def main():
         variants = {"coop": ("1", "1"), "2k": ("1", "0"), "4k": ("0", "0")}
         for _ in range(reps):
             for name, (fused, coop) in variants.items():
-                os.environ["SK_CG_FUSED"] = fused
-                os.environ["SK_CG_COOP"] = coop
+                _lib.set_option("cg_fused", int(fused))
+                _lib.set_option("cg_coop", int(coop))
                 s = DeviceStencil(bilaplacian(2))  # a new plan with this setting (one cached plan per thread)
                 try:
                     cg_solve_stencil(s, g, b, o)  # untimed: plan, graph

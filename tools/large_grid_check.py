@@ -39,7 +39,7 @@ def main():
     c0 = 0.05 * rng.uniform(-1, 1, g.unknown_count())
     out = {}
     for flag in ("1", "0"):
-        os.environ["SK_CH_PADDED"] = flag
+        _lib.set_option("ch_padded", int(flag))
         st = CahnHilliardExplicit(g, p)
         c, s = DeviceArray.from_host(c0), DeviceArray(g.unknown_count())
         m0 = dsum(c)
