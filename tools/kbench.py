@@ -56,7 +56,7 @@ def main():
         dim = 3 if case.startswith("ch3d") else 2
         n = args.n or (256 if dim == 3 else 2048)
         eps = 0.02 if dim == 3 else 0.01
-        form = {"c": "composed", "p": "probe-copy"}.get(case[-1], "factored")
+        form = "composed" if case.endswith("c") else "factored"
         p = CahnHilliardParams.from_epsilon(eps, form)
         h = 1.0 / n
         dt = (0.2 * h ** 4 / (144 * eps * eps)) if dim == 3 else (0.25 * h ** 4 / (64 * eps * eps))
