@@ -117,12 +117,15 @@ def load(path: Optional[Path] = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = Path(path) if path is not None else LIB_PATH
+    explicit = path is not None
+    path = Path(path) if explicit else LIB_PATH
     if not path.exists():
         raise RuntimeError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                            "(the CUDA path has no CPU fallback)")
     lib = C.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
+        if explicit and not hasattr(lib, name):  # an older A/B build may lack newer entry points
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -77,7 +77,9 @@ struct ChfSmem {
   static constexpr int MP = C::TX + 4;              // mu ring pitch: x in [-1, TX] at column x + 2
   static constexpr int MU_ROWS = C::TY + 2;         // y in [-1, TY]
   static constexpr int MU_PLANE = MU_ROWS * MP;
-  static constexpr int MU_SLOTS = SK_MU_SLOTS;     // 2: slot parity (written at step k, read at k+1)
+  // 3: slot = plane % 3 (static roles); 4 (TMA path): rotating slots, which
+  // lets the step barrier's wait move after the mu write (more slack)
+  static constexpr int MU_SLOTS = LD ? SK_MU_SLOTS : 3;
   // LD 0 with the 8-byte fallback loader (FB): its boundary-map table after the mu ring
   static constexpr int TAB = C::STAGES * PLANE + MU_SLOTS * MU_PLANE;  // doubles from the ring
   static constexpr int BYTES = RING_OFS + TAB * 8 + (FB ? C::TABLE_BYTES : 0);
@@ -85,7 +87,7 @@ struct ChfSmem {
   static constexpr int BORDER_ROWS = 2 * (C::TX + 2);                     // mu rows -1 and TY, x in [-1, TX]
   static constexpr int ROWS_PER_WARP = (BORDER_ROWS + WARPS - 1) / WARPS;  // + 4 side points per warp
   static_assert(ROWS_PER_WARP + 4 <= 32, "border points per warp");
-  static_assert(!LD || (STAGE_BYTES % 128 == 0 && C::STAGES * 8 <= 128), "TMA stage alignment");
+  static_assert(!LD || (STAGE_BYTES % 128 == 0 && (C::STAGES + 3) * 8 <= 128), "TMA stage alignment + step barriers");
   static_assert(!LD || (C::ROWS % kTmaSplit == 0 && (C::ROWS / kTmaSplit) * P * 8 % 128 == 0), "TMA box split");
 };
 
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   } else {
     if (threadIdx.x == 0) {
       for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+      for (int i = 0; i < 3; ++i) mbar_init(&bars[S + i], C::THREADS / 32);  // step barriers: one arrival per warp
       fence_mbar_init();
     }
     __syncthreads();
@@ -204,7 +207,20 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   double Cz[3][4], M[3][4];  // own c of plane j in Cz[j % 3], own mu of plane j in M[j % 3]; point 2 * row + col
   int s_k = 0;               // stage of c-plane k
   uint32_t ph = 0;           // LD 1: parity of the current use of stage s_k
-  int mpar = 0;              // MU_SLOTS 2: mu slot of plane k-1
+  int ms = 0;                // MU_SLOTS 4: mu slot of plane k-1 (plane k-2: ms - 1 mod 4)
+  constexpr bool kLateWait = SM::MU_SLOTS >= 4;
+  // LD 1: split-phase step barrier instead of __syncthreads. Every warp
+  // arrives on step barrier t % 3 once its mu slot and border points of step
+  // t are written (its reads of the c stages of step t are done by then),
+  // and waits for step t-1's barrier after loading its own c of step t,
+  // before it overwrites the mu slot its neighbours read in step t-2: the
+  // output of step t-1 (computed after that arrival) is the slack, so warps
+  // drift instead of idling at a full-CTA barrier. Three rotating barriers
+  // (the mu ring's three slots) keep every reuse ordered transitively.
+  uint64_t* stepbar = bars + S;
+  int sb = 0;                // t % 3
+  uint32_t sph = 0;          // (t / 3) & 1
+  bool started = false;      // t > 0
   for (int u = ubeg; u < uend; ) {
     const Seg sg = seg_of<C>(a, u, uend);
     u += sg.len;
@@ -228,17 +244,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       constexpr int M1 = (K + 2) % 3, M2 = (K + 1) % 3, M3 = K;  // mu of planes k-1, k-2, k-3
       (void)M2;
       (void)M3;
+      const int s_iss = s_load;  // LD 1: the stage refilled in this step (plane k-3's)
       if constexpr (LD == 0) {
         cp_async_wait_group<S - 4>();
         __syncthreads();
         lc.issue_next(ring, s_load, a);
       } else {
         mbar_wait(&bars[s_k], ph);  // plane k landed
-        __syncthreads();            // ... and stage (k - 3) is free, the mu slot of plane k-2 complete
-        if (threadIdx.x == 0) {
-          fence_proxy_async_smem();
-          tc.issue_next(ring, bars, s_load, a, &tmap);
-        }
       }
       s_load = s_load + 1 == S ? 0 : s_load + 1;
       const int s_k1 = s_k == 0 ? S - 1 : s_k - 1;   // stage of plane k-1
@@ -252,9 +264,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       // only depend on the previous step's mu slot and the own mu registers
       double olf0 = 0, olf1 = 0, ort0 = 0, ort1 = 0;
       double2 oup = make_double2(0, 0), odn = make_double2(0, 0);
-      if constexpr (DO_OUT && V == 0) {
+      auto out_neighbours = [&]() {
         const double* m2 = M[M2];
-        const double* mb = mu_ring + (SM::MU_SLOTS == 2 ? (mpar ^ 1) : M2) * SM::MU_PLANE + mofs;  // plane k-2
+        const double* mb = mu_ring + (SM::MU_SLOTS == 3 ? M2 : (ms == 0 ? SM::MU_SLOTS - 1 : ms - 1)) * SM::MU_PLANE + mofs;  // plane k-2
         olf0 = __shfl_up_sync(0xffffffffu, m2[1], 1);
         olf1 = __shfl_up_sync(0xffffffffu, m2[3], 1);
         ort0 = __shfl_down_sync(0xffffffffu, m2[0], 1);
@@ -263,6 +275,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         if (lane == 31) { ort0 = mb[2]; ort1 = mb[MP + 2]; }
         oup = ld2(mb - MP);
         odn = ld2(mb + 2 * MP);
+      };
+      if constexpr (DO_OUT && V == 0 && LD == 0) out_neighbours();
+      if constexpr (LD == 1 && !kLateWait) {  // all warps past step t-1: the mu slot written below is free
+        if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
       }
       if constexpr (DO_MU && V == 1) {
 #pragma unroll
@@ -288,9 +304,39 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         m1[1] = fma(a.kl1, s01, fma(a.kl0, c1[1], poly3(c1[1], a.chem)));
         m1[2] = fma(a.kl1, s10, fma(a.kl0, c1[2], poly3(c1[2], a.chem)));
         m1[3] = fma(a.kl1, s11, fma(a.kl0, c1[3], poly3(c1[3], a.chem)));
-        double* mb = mu_ring + (SM::MU_SLOTS == 2 ? mpar : M1) * SM::MU_PLANE + mofs;  // plane k-1
+        double* mb = mu_ring + (SM::MU_SLOTS == 3 ? M1 : ms) * SM::MU_PLANE + mofs;  // plane k-1
         *reinterpret_cast<double2*>(mb) = make_double2(m1[0], m1[1]);
         *reinterpret_cast<double2*>(mb + MP) = make_double2(m1[2], m1[3]);
+      }
+      auto border_mu = [&]() {
+        if constexpr (DO_MU && V == 0) {
+          if (has_ex) {  // one border point of the mu tile (needed from the next step on)
+            const double* rb = ring + s_k1 * PLANE + ex_c;
+            const double cc = rb[0];
+            const double sr =
+                (((rb[-1] + rb[1]) + (rb[-P] + rb[P])) + ring[s_k2 * PLANE + ex_c]) + ring[s_k * PLANE + ex_c];
+            mu_ring[(SM::MU_SLOTS == 3 ? M1 : ms) * SM::MU_PLANE + ex_m] =
+                fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
+          }
+        }
+      };
+      if constexpr (LD == 1) {
+        border_mu();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stepbar[sb]);  // this warp is done with step t's stages and mu slot
+        if constexpr (kLateWait) {  // 4 mu slots: the slot written above was last read in step t-3
+          if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
+        }
+        if (threadIdx.x == 0) {  // stage of plane k-3 is free (last read at step t-1)
+          fence_proxy_async_smem();
+          tc.issue_next(ring, bars, s_iss, a, &tmap);
+        }
+        if constexpr (DO_OUT && V == 0) out_neighbours();
+        started = true;
+        if (++sb == 3) {
+          sb = 0;
+          sph ^= 1u;
+        }
       }
       if constexpr (DO_OUT) {  // output plane k-2
         const double* c2 = Cz[C2];
@@ -338,20 +384,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         }
         outp += opp;
       }
-      if constexpr (DO_MU && V == 0) {
-        if (has_ex) {  // one border point of the mu tile (needed from the next step on)
-          const double* rb = ring + s_k1 * PLANE + ex_c;
-          const double cc = rb[0];
-          const double sr =
-              (((rb[-1] + rb[1]) + (rb[-P] + rb[P])) + ring[s_k2 * PLANE + ex_c]) + ring[s_k * PLANE + ex_c];
-          mu_ring[(SM::MU_SLOTS == 2 ? mpar : M1) * SM::MU_PLANE + ex_m] = fma(a.kl1, sr, fma(a.kl0, cc, poly3(cc, a.chem)));
-        }
-      }
+      if constexpr (LD == 0) border_mu();
       if (++s_k == S) {
         s_k = 0;
         ph ^= 1u;
       }
-      mpar ^= 1;
+      if constexpr (SM::MU_SLOTS != 3) ms = ms + 1 == SM::MU_SLOTS ? 0 : ms + 1;
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;

@@ -33,7 +33,10 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--ks", default="1,2,3,20,52,102")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--lib", default=None, help="alternative build (tools/ab_build.py)")
     args = ap.parse_args()
+    if args.lib:
+        _lib.load(Path(args.lib))
     lib = _lib.ensure_device(0)
     n = args.n
     eps = 0.02

@@ -46,7 +46,10 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--steps", type=int, default=2, help="CH steps per timed call (>= 100: graph chunks)")
+    ap.add_argument("--lib", default=None, help="alternative build (tools/ab_build.py)")
     args = ap.parse_args()
+    if args.lib:
+        _lib.load(Path(args.lib))
     lib = _lib.ensure_device(0)
     rng = np.random.default_rng(0)
     case = args.case
