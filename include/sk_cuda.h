@@ -294,6 +294,34 @@ int sk_cg_solve_host(const sk_csr* m, const double* b_host, double* x_host,
 int sk_cg_solve_stencil(const sk_stencil* s, const sk_grid_desc* g, const double* b_dev, double* x_dev,
                         const sk_solve_options* opts, sk_solve_report* report, void* stream);
 
+/* ---- exact-operator refinement (configs 2 / 5; no reference symbol) ------
+ * The doubles of non-dyadic composed weights do not sum to zero (73-point:
+ * -2.6e-15), a zeroth-order perturbation of size |sum| h^s that pollutes the
+ * manufactured solution at fine grids. sk_stencil_create_exact
+ * also takes coeff_lo[e] = coefficient_e - coeff[e] (the rounding error of
+ * Rational::to_double, rational.hpp:32, as a double), so coeff + coeff_lo is
+ * the exact rational to ~2^-106; every other entry point still uses coeff
+ * (the reference's fp64 matrix). sk_residual_refined: r = b - A x with the
+ * exact weights, evaluated in double-double (error-free products and
+ * compensated sums), rounded to fp64. sk_cg_solve_stencil_refined: the
+ * matrix-free CG (opts) followed by up to max_refinements steps
+ * x += CG(A_fl, r_refined) with inner tolerance inner_rel_tol (recurrence
+ * criterion), stopping when ||d|| <= 1e-15 ||x||. */
+typedef struct sk_refine_report {
+  int64_t iterations;               /* CG iterations, all solves */
+  int refinements;                  /* correction steps taken */
+  double initial_true_rel_residual; /* fp64-operator true residual of the first CG solve */
+  double refined_rel_residual;      /* ||b - A_exact x|| / ||b|| (double-double) at return */
+  double last_correction_rel;       /* ||d|| / ||x|| of the last correction */
+} sk_refine_report;
+int sk_stencil_create_exact(int dim, int nent, const int32_t* offsets, const double* coeff,
+                            const double* coeff_lo, int h_power, sk_stencil** out);
+int sk_residual_refined(const sk_stencil* s, const sk_grid_desc* g, const double* b_dev,
+                        const double* x_dev, double* r_dev, void* stream);
+int sk_cg_solve_stencil_refined(const sk_stencil* s, const sk_grid_desc* g, const double* b_dev,
+                                double* x_dev, const sk_solve_options* opts, double inner_rel_tol,
+                                int max_refinements, sk_refine_report* report, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

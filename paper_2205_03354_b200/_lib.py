@@ -38,6 +38,11 @@ class SolveOptionsC(C.Structure):
                 ("accept_recurrence", c_int), ("use_initial_guess", c_int)]
 
 
+class RefineReportC(C.Structure):
+    _fields_ = [("iterations", c_i64), ("refinements", c_int), ("initial_true_rel_residual", c_dbl),
+                ("refined_rel_residual", c_dbl), ("last_correction_rel", c_dbl)]
+
+
 class SolveReportC(C.Structure):
     _fields_ = [("iterations", c_i64), ("restarts", c_i64), ("true_rel_residual", c_dbl),
                 ("recurrence_rel_residual", c_dbl)]
@@ -105,6 +110,10 @@ SIGNATURES = {
     "sk_cg_solve_host": (c_int, [vp, vp, vp, C.POINTER(SolveOptionsC), C.POINTER(SolveReportC)]),
     "sk_cg_solve_stencil": (c_int, [vp, C.POINTER(GridDesc), vp, vp, C.POINTER(SolveOptionsC), C.POINTER(SolveReportC),
                                     vp]),
+    "sk_stencil_create_exact": (c_int, [c_int, c_int, vp, vp, vp, c_int, C.POINTER(vp)]),
+    "sk_residual_refined": (c_int, [vp, C.POINTER(GridDesc), vp, vp, vp, vp]),
+    "sk_cg_solve_stencil_refined": (c_int, [vp, C.POINTER(GridDesc), vp, vp, C.POINTER(SolveOptionsC), c_dbl, c_int,
+                                            C.POINTER(RefineReportC), vp]),
 }
 
 _lib: Optional[C.CDLL] = None

@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 LIB = PKG / "libsk_cuda.so"
 
-SOURCES = ["sk_common.cu", "sk_stencil.cu", "sk_ch.cu", "sk_blas.cu", "sk_csr.cu", "sk_cg.cu", "sk_imex.cu", "sk_spectral.cu", "sk_matmul.cu"]
+SOURCES = ["sk_common.cu", "sk_stencil.cu", "sk_ch.cu", "sk_blas.cu", "sk_csr.cu", "sk_cg.cu", "sk_imex.cu", "sk_spectral.cu", "sk_matmul.cu", "sk_refine.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3",

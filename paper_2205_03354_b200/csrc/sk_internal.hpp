@@ -26,6 +26,11 @@ struct sk_stencil {
   double orbit_coeff[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int* d_off = nullptr;       // device copy for the generic kernel / assembly
   double* d_coeff = nullptr;
+  // exact-weight correction (sk_stencil_create_exact): coeff + coeff_lo is the
+  // exact rational coefficient to ~2^-106 relative; used only by the refined
+  // residual (sk_residual_refined). Empty: corrections are zero.
+  std::vector<double> coeff_lo;
+  double* d_coeff_lo = nullptr;
   // cached CUDA graph of sk_composed_apply_repeat: the captured kernels bake
   // in the buffers, the grid (extents, boundary kinds, h -> weights) and the
   // option epoch, all part of the key; rep_mu serialises concurrent callers

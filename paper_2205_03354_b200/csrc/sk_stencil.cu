@@ -23,6 +23,7 @@ sk_stencil::~sk_stencil() {
   if (rep_exec) cudaGraphExecDestroy(rep_exec);
   if (d_off) cudaFree(d_off);
   if (d_coeff) cudaFree(d_coeff);
+  if (d_coeff_lo) cudaFree(d_coeff_lo);
 }
 
 namespace sk {

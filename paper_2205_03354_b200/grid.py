@@ -8,6 +8,7 @@ reference lacks (its apply is always assemble + csr_matvec, grid.cpp:166-172).
 from __future__ import annotations
 
 import ctypes as C
+from fractions import Fraction
 import enum
 from dataclasses import dataclass, field
 from typing import List, Optional, Tuple
@@ -92,10 +93,14 @@ class DeviceStencil:
         self.lib = ensure_device()
         self.stencil = s
         offs, coeffs = s.flat()
+        # exact-weight corrections (only the refined residual uses them):
+        # coefficient - to_double(coefficient), exactly, rounded once
+        lows = [float(q - Fraction(d)) for q, d in zip(s.entries.values(), coeffs)]
         o = (C.c_int32 * len(offs))(*offs)
         c = (C.c_double * len(coeffs))(*coeffs)
+        lo = (C.c_double * len(lows))(*lows)
         h = C.c_void_p()
-        check(self.lib.sk_stencil_create(s.dim, len(coeffs), o, c, s.h_power, C.byref(h)))
+        check(self.lib.sk_stencil_create_exact(s.dim, len(coeffs), o, c, lo, s.h_power, C.byref(h)))
         self.handle = h.value
 
     @property
@@ -219,3 +224,14 @@ def composed_apply_repeat(s, g: GridSpec, u: DeviceArray, v0: DeviceArray, v1: D
     ds = as_device_stencil(s)
     d = g.desc()
     check(ds.lib.sk_composed_apply_repeat(ds.handle, C.byref(d), u.ptr, v0.ptr, v1.ptr, repeats, stream))
+
+
+def residual_refined(s, g: GridSpec, b, x) -> np.ndarray:
+    """b - A x with the composed stencil's EXACT weights, in double-double (sk_residual_refined)."""
+    ds = as_device_stencil(s)
+    db, hb = _as_device(b)
+    dx, _ = _as_device(x)
+    r = DeviceArray(g.unknown_count())
+    d = g.desc()
+    check(ds.lib.sk_residual_refined(ds.handle, C.byref(d), db.ptr, dx.ptr, r.ptr, None))
+    return r.to_host() if hb else r

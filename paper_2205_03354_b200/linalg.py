@@ -135,3 +135,42 @@ def periodic_spectrum(stencil, grid, affine_shift: float = 0.0, affine_scale: fl
     check(ds.lib.sk_periodic_spectrum(ds.handle, C.byref(d), affine_shift, affine_scale, ev.ctypes.data,
                                       C.byref(rho), C.byref(sym), C.byref(cond)))
     return SpectrumReport(ev.view(np.complex128), rho.value, sym.value, cond.value)
+
+
+@dataclass
+class RefineReport:
+    """sk_refine_report: CG iterations over all solves, refinement steps, the
+    first solve's fp64 true residual, the exact-operator residual at return and
+    the last correction's relative size."""
+    iterations: int = 0
+    refinements: int = 0
+    initial_true_rel_residual: float = float("nan")
+    refined_rel_residual: float = float("nan")
+    last_correction_rel: float = float("nan")
+
+
+def cg_solve_stencil_refined(stencil, grid, b, opts: SolveOptions | None = None, inner_rel_tol: float = 1e-6,
+                             max_refinements: int = 4, report: RefineReport | None = None,
+                             x_out: DeviceArray | None = None, stream=None):
+    """Matrix-free CG, then iterative refinement against the exact composed
+    operator (double-double residual): x converges to the solution of the
+    exact-rational system instead of the fp64-weight one (sk_cg_solve_stencil_refined)."""
+    from ._lib import RefineReportC
+    from .grid import as_device_stencil
+
+    opts = opts or SolveOptions()
+    ds = as_device_stencil(stencil)
+    d = grid.desc()
+    rows = grid.unknown_count()
+    rep = RefineReportC()
+    o = _opts(opts)
+    host = not isinstance(b, DeviceArray)
+    db = DeviceArray.from_host(np.ascontiguousarray(b, np.float64)) if host else b
+    x = x_out if x_out is not None else DeviceArray(rows)
+    check(ds.lib.sk_cg_solve_stencil_refined(ds.handle, C.byref(d), db.ptr, x.ptr, C.byref(o), inner_rel_tol,
+                                             max_refinements, C.byref(rep), stream))
+    if report is not None:
+        report.iterations, report.refinements = rep.iterations, rep.refinements
+        report.initial_true_rel_residual = rep.initial_true_rel_residual
+        report.refined_rel_residual, report.last_correction_rel = rep.refined_rel_residual, rep.last_correction_rel
+    return x.to_host() if host else x

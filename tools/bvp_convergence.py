@@ -37,7 +37,8 @@ from paper_2205_03354_b200.device import DeviceArray  # noqa: E402
 from paper_2205_03354_b200.errors import StencilkitError  # noqa: E402
 from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, assemble, make_grid  # noqa: E402
 from paper_2205_03354_b200.experiments import fit_loglog  # noqa: E402
-from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve, cg_solve_stencil  # noqa: E402
+from paper_2205_03354_b200.linalg import (RefineReport, SolveOptions, SolveReport, cg_solve,  # noqa: E402
+                                          cg_solve_stencil, cg_solve_stencil_refined)
 from paper_2205_03354_b200.stencil import bilaplacian  # noqa: E402
 
 
@@ -96,6 +97,10 @@ def main() -> None:
     ap.add_argument("--index-bits", type=int, default=64)
     ap.add_argument("--matrix-free", action="store_true",
                     help="CG on the stencil operator (sk_cg_solve_stencil) instead of the assembled CSR")
+    ap.add_argument("--refine", type=int, default=0,
+                    help="iterative refinement steps against the exact composed operator (matrix-free; "
+                         "sk_cg_solve_stencil_refined)")
+    ap.add_argument("--inner-rtol", type=float, default=1e-6, help="CG tolerance of each refinement correction")
     args = ap.parse_args()
     lib = _lib.ensure_device(0)
     s = DeviceStencil(bilaplacian(args.dim, args.acc))
@@ -103,7 +108,7 @@ def main() -> None:
     for N in args.ladder:
         g = make_grid(args.dim, N + 1, 1.0 / N, BoundaryKind.clamped)
         t0 = time.perf_counter()
-        m = None if args.matrix_free else assemble(s, g, index_bits=args.index_bits)
+        m = None if (args.matrix_free or args.refine) else assemble(s, g, index_bits=args.index_bits)
         t_asm = time.perf_counter() - t0
         rows = g.unknown_count()
         f, u = manufactured(args.dim, N)
@@ -115,10 +120,15 @@ def main() -> None:
         opts = SolveOptions(rel_tol=args.rtol, max_iter=args.max_iter, check_every=256,
                             accept_recurrence=not args.reference_criterion, use_initial_guess=use_x0)
         rep = SolveReport()
+        rrep = RefineReport()
         status = "ok"
         t0 = time.perf_counter()
         try:
-            if m is None:
+            if args.refine:
+                cg_solve_stencil_refined(s, g, b, opts, args.inner_rtol, args.refine, rrep, x_out=x)
+                rep.iterations = rrep.iterations
+                rep.true_rel_residual = rrep.initial_true_rel_residual
+            elif m is None:
                 cg_solve_stencil(s, g, b, opts, rep, x_out=x)
             else:
                 cg_solve(m, b, opts, rep, x_out=x)
@@ -135,12 +145,17 @@ def main() -> None:
                           "ms_per_iteration": round(1e3 * t_cg / max(rep.iterations, 1), 4),
                           "true_rel_residual": rep.true_rel_residual,
                           "recurrence_rel_residual": rep.recurrence_rel_residual, "max_error": err,
-                          "nested_x0": use_x0, "status": status}), flush=True)
+                          "nested_x0": use_x0, "status": status,
+                          **({"refinements": rrep.refinements, "refined_rel_residual": rrep.refined_rel_residual,
+                              "last_correction_rel": rrep.last_correction_rel} if args.refine else {})}),
+              flush=True)
         del m, b, x
     if len(samples) >= 3:
         fit = fit_loglog(samples)
+        pairs = [math.log(samples[i][1] / samples[i + 1][1]) / math.log(samples[i][0] / samples[i + 1][0])
+                 for i in range(len(samples) - 1)]
         print(json.dumps({"fit": {"slope": fit.slope, "coefficient": fit.coefficient, "fit_residual": fit.fit_residual},
-                          "samples": samples}), flush=True)
+                          "pairwise_orders": pairs, "samples": samples}), flush=True)
 
 
 if __name__ == "__main__":
