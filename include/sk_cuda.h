@@ -301,7 +301,9 @@ int sk_cg_solve_stencil(const sk_stencil* s, const sk_grid_desc* g, const double
  * also takes coeff_lo[e] = coefficient_e - coeff[e] (the rounding error of
  * Rational::to_double, rational.hpp:32, as a double), so coeff + coeff_lo is
  * the exact rational to ~2^-106; every other entry point still uses coeff
- * (the reference's fp64 matrix). sk_residual_refined: r = b - A x with the
+ * (the reference's fp64 matrix). The grid scale is pow_int(h, h_power) as
+ * the reference computes it (exact for the configs' dyadic h).
+ * sk_residual_refined: r = b - A x with the
  * exact weights, evaluated in double-double (error-free products and
  * compensated sums), rounded to fp64. sk_cg_solve_stencil_refined: the
  * matrix-free CG (opts) followed by up to max_refinements steps
