@@ -256,6 +256,10 @@ int sk_periodic_spectrum(const sk_stencil* s, const sk_grid_desc* g, double affi
 /* ---- CSR assembly (grid.cpp:62-158) and SpMV (kernels.cpp:8-17) --------- */
 int sk_csr_assemble(const sk_stencil* s, const sk_grid_desc* g, int index_bits, sk_csr** out,
                     void* stream);
+/* Re-assemble into an existing matrix of the same rows / nonzero count (no
+ * allocation; e.g. new weights after an h change): SK_ERR_SHAPE_MISMATCH
+ * otherwise. Cached solver plans of the matrix are invalidated. */
+int sk_csr_assemble_into(const sk_stencil* s, const sk_grid_desc* g, sk_csr* m, void* stream);
 int sk_csr_upload(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
                   const int64_t* col_idx, const double* values, int index_bits, sk_csr** out);
 int sk_csr_info(const sk_csr* m, int64_t* rows, int64_t* cols, int64_t* nnz, int* index_bits);

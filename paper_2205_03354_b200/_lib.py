@@ -94,6 +94,7 @@ SIGNATURES = {
     "sk_power_iteration": (c_int, [vp, c_dbl, C.c_uint64, c_i64, pd, C.POINTER(c_i64), vp]),
     "sk_periodic_spectrum": (c_int, [vp, C.POINTER(GridDesc), c_dbl, c_dbl, vp, pd, pd, pd]),
     "sk_csr_assemble": (c_int, [vp, C.POINTER(GridDesc), c_int, C.POINTER(vp), vp]),
+    "sk_csr_assemble_into": (c_int, [vp, C.POINTER(GridDesc), vp, vp]),
     "sk_csr_upload": (c_int, [c_i64, c_i64, c_i64, vp, vp, vp, c_int, C.POINTER(vp)]),
     "sk_csr_info": (c_int, [vp, C.POINTER(c_i64), C.POINTER(c_i64), C.POINTER(c_i64), C.POINTER(c_int)]),
     "sk_csr_download": (c_int, [vp, vp, vp, vp]),

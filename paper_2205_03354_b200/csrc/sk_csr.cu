@@ -266,7 +266,7 @@ struct AsmTables {
   const int* interior;      // [3][16]
   const int64_t* tnnz;      // [ntmpl]
   const int64_t* toff;      // [ntmpl] first slot
-  const int4* tcomp;        // [nslots] comp_rel (x,y,z)
+  const int64_t* tcol;      // [nslots] column of the slot relative to the row's base column
   const double* tval;       // [nslots]
   const int64_t* cum0;      // [ntmpl]
   const int64_t* t1;        // [nc1*nc2]
@@ -283,26 +283,38 @@ __device__ __forceinline__ int axis_class(const AsmTables& t, int a, int64_t i) 
   return t.rl[a];
 }
 
+// One warp per 32 consecutive rows. Row phase (lane = row): the row's
+// boundary-class template, its closed-form row pointer, and two per-row
+// constants in shared memory: base = the column offset of the row's interior
+// axes, sofs = template slot of the row's first entry minus its row pointer.
+// Element phase (lane = entry, coalesced over the warp's contiguous entry
+// range): find the row by a 5-step search over the 33 row pointers, then
+// col = tcol[sofs + e] + base and val = tval[sofs + e] — two L1-resident
+// table reads and two streaming stores per nonzero, no integer division.
 template <class IDX>
 __global__ void __launch_bounds__(256) assemble_kernel(const AsmTables t, int64_t* __restrict__ row_ptr,
                                                        IDX* __restrict__ col_idx, double* __restrict__ values) {
   __shared__ int64_t s_rp[8][33];
-  __shared__ int s_t[8][32];
+  __shared__ int64_t s_base[8][32];
+  __shared__ int64_t s_sofs[8][32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t r0 = (int64_t(blockIdx.x) * 8 + warp) * 32;
   if (r0 >= t.rows) return;
   const int64_t r = r0 + lane;
-  int64_t rp = 0, nnz = 0;
-  int tid = 0;
+  int64_t rp = 0, nnz = 0, base = 0, sofs = 0;
   if (r < t.rows) {
-    const int64_t i0 = r % t.un[0], i1 = (r / t.un[0]) % t.un[1], i2 = r / (t.un[0] * t.un[1]);
+    const int64_t q = r / t.un[0];
+    const int64_t i0 = r - q * t.un[0], i2 = q / t.un[1], i1 = q - i2 * t.un[1];
     const int c0 = axis_class(t, 0, i0), c1 = axis_class(t, 1, i1), c2 = axis_class(t, 2, i2);
     const int c12 = c2 * t.ncls[1] + c1;
-    tid = c12 * t.ncls[0] + c0;
+    const int tid = c12 * t.ncls[0] + c0;
     nnz = __ldg(t.tnnz + tid);
     rp = __ldg(t.cum0 + tid) + (i0 - __ldg(t.start + 0 * 16 + c0)) * nnz + __ldg(t.cum1 + c12) +
          (i1 - __ldg(t.start + 1 * 16 + c1)) * __ldg(t.t1 + c12) + __ldg(t.cum2 + c2) +
          (i2 - __ldg(t.start + 2 * 16 + c2)) * __ldg(t.t2 + c2);
+    base = (__ldg(t.interior + 0 * 16 + c0) ? i0 : 0) +
+           t.un[0] * ((__ldg(t.interior + 1 * 16 + c1) ? i1 : 0) + t.un[1] * (__ldg(t.interior + 2 * 16 + c2) ? i2 : 0));
+    sofs = __ldg(t.toff + tid) - rp;
     row_ptr[r] = rp;
     if (r == t.rows - 1) row_ptr[t.rows] = rp + nnz;
   }
@@ -310,7 +322,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmTables t, int64_
   const int last = t.rows - 1 - r0 < 31 ? int(t.rows - 1 - r0) : 31;
   const int64_t end = __shfl_sync(0xffffffffu, rp + nnz, last);
   s_rp[warp][lane] = r < t.rows ? rp : end;
-  s_t[warp][lane] = tid;
+  s_base[warp][lane] = base;
+  s_sofs[warp][lane] = sofs;
   if (lane == 0) s_rp[warp][32] = end;
   __syncwarp();
   const int64_t begin = s_rp[warp][0];
@@ -321,28 +334,23 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmTables t, int64_
       const int mid = (lo + hi) >> 1;
       if (s_rp[warp][mid] <= e) lo = mid; else hi = mid;
     }
-    const int j = lo;
-    const int64_t row = r0 + j;
-    const int tj = s_t[warp][j];
-    const int64_t slot = __ldg(t.toff + tj) + (e - s_rp[warp][j]);
-    const int64_t i0 = row % t.un[0], i1 = (row / t.un[0]) % t.un[1], i2 = row / (t.un[0] * t.un[1]);
-    const int c0 = axis_class(t, 0, i0), c1 = axis_class(t, 1, i1), c2 = axis_class(t, 2, i2);
-    const int4 cr = __ldg(t.tcomp + slot);
-    const int64_t x = cr.x + (__ldg(t.interior + 0 * 16 + c0) ? i0 : 0);
-    const int64_t y = cr.y + (__ldg(t.interior + 1 * 16 + c1) ? i1 : 0);
-    const int64_t z = cr.z + (__ldg(t.interior + 2 * 16 + c2) ? i2 : 0);
-    col_idx[e] = IDX(x + t.un[0] * (y + t.un[1] * z));
-    values[e] = __ldg(t.tval + slot);
+    const int64_t slot = s_sofs[warp][lo] + e;
+    __stcs(col_idx + e, IDX(__ldg(t.tcol + slot) + s_base[warp][lo]));
+    __stcs(values + e, __ldg(t.tval + slot));
   }
 }
 
-}  // namespace
+// Host half of the assembly: the reference row algorithm once per boundary
+// class tuple (reference_row), the slot tables and the closed-form row
+// pointers, packed into one device blob.
+struct AsmPlan {
+  std::vector<unsigned char> blob;
+  size_t o_start, o_int, o_tnnz, o_toff, o_tcol, o_tval, o_cum0, o_t1, o_cum1, o_t2, o_cum2;
+  int64_t total = 0;
+  AsmTables t{};
+};
 
-int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr** out, cudaStream_t stream) {
-  if (int st = check_width(s, g)) return st;
-  if (index_bits != 32 && index_bits != 64) return fail(SK_ERR_INVALID_ARGUMENT, "index_bits must be 32 or 64");
-  if (index_bits == 32 && g.rows > int64_t(INT32_MAX)) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for int32 columns");
-  // classes per axis
+int asm_plan(const sk_stencil* s, const GridInfo& g, AsmPlan* P) {
   AxisClasses ac[3];
   for (int a = 0; a < 3; ++a) ac[a] = axis_classes(g.un[a], s->lo[a], s->hi[a], a < g.dim);
   for (int a = 0; a < 3; ++a)
@@ -355,7 +363,7 @@ int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr*
   for (int e = 0; e < s->nent; ++e) wval[size_t(e)] = s->coeff[size_t(e)] * scale;
 
   std::vector<int64_t> tnnz(static_cast<size_t>(ntmpl)), toff(static_cast<size_t>(ntmpl));
-  std::vector<int4> tcomp;
+  std::vector<int64_t> tcol;
   std::vector<double> tval;
   for (int c2 = 0; c2 < n2; ++c2)
     for (int c1 = 0; c1 < n1; ++c1)
@@ -372,9 +380,9 @@ int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr*
           for (int a = 0; a < 3; ++a) {
             comp[a] = rem % g.un[a];
             rem /= g.un[a];
-            if (ac[a].interior[size_t(cls[a])]) comp[a] -= rep[a];
+            if (ac[a].interior[size_t(cls[a])]) comp[a] -= rep[a];  // relative to the row on interior axes
           }
-          tcomp.push_back(make_int4(int(comp[0]), int(comp[1]), int(comp[2]), 0));
+          tcol.push_back(comp[0] + g.un[0] * (comp[1] + g.un[1] * comp[2]));
           tval.push_back(v);
         }
       }
@@ -402,8 +410,6 @@ int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr*
     cum2[size_t(c2)] = total;
     total += ac[2].size[size_t(c2)] * acc;
   }
-
-  // table buffer
   std::vector<int64_t> start(48, 0);
   std::vector<int> interior(48, 0);
   for (int a = 0; a < 3; ++a)
@@ -412,38 +418,29 @@ int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr*
       interior[size_t(a * 16 + c)] = ac[a].interior[size_t(c)];
     }
   const size_t nslots = std::max<size_t>(tval.size(), 1);
-  std::vector<unsigned char> blob;
+  auto& blob = P->blob;
+  blob.clear();
   auto put = [&](const void* p, size_t bytes) {
     size_t off = (blob.size() + 15) & ~size_t(15);
     blob.resize(off + bytes);
     if (bytes) std::memcpy(blob.data() + off, p, bytes);
     return off;
   };
-  tcomp.resize(nslots, make_int4(0, 0, 0, 0));
+  tcol.resize(nslots, 0);
   tval.resize(nslots, 0.0);
-  const size_t o_start = put(start.data(), start.size() * 8), o_int = put(interior.data(), interior.size() * 4),
-               o_tnnz = put(tnnz.data(), tnnz.size() * 8), o_toff = put(toff.data(), toff.size() * 8),
-               o_tcomp = put(tcomp.data(), tcomp.size() * sizeof(int4)), o_tval = put(tval.data(), tval.size() * 8),
-               o_cum0 = put(cum0.data(), cum0.size() * 8), o_t1 = put(t1.data(), t1.size() * 8),
-               o_cum1 = put(cum1.data(), cum1.size() * 8), o_t2 = put(t2.data(), t2.size() * 8),
-               o_cum2 = put(cum2.data(), cum2.size() * 8);
-
-  auto* m = new sk_csr;
-  m->rows = m->cols = g.rows;
-  m->nnz = total;
-  m->index_bits = index_bits;
-  unsigned char* d_blob = nullptr;
-  cudaError_t e = cudaMalloc(&m->row_ptr, sizeof(int64_t) * size_t(g.rows + 1));
-  if (e == cudaSuccess && total > 0) e = cudaMalloc(&m->col, size_t(total) * (index_bits / 8));
-  if (e == cudaSuccess && total > 0) e = cudaMalloc(&m->val, sizeof(double) * size_t(total));
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_blob), blob.size(), stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) {
-    if (d_blob) cudaFreeAsync(d_blob, stream);
-    delete m;
-    return cuda_fail(e, "csr_assemble allocation");
-  }
-  AsmTables t{};
+  P->o_start = put(start.data(), start.size() * 8);
+  P->o_int = put(interior.data(), interior.size() * 4);
+  P->o_tnnz = put(tnnz.data(), tnnz.size() * 8);
+  P->o_toff = put(toff.data(), toff.size() * 8);
+  P->o_tcol = put(tcol.data(), tcol.size() * 8);
+  P->o_tval = put(tval.data(), tval.size() * 8);
+  P->o_cum0 = put(cum0.data(), cum0.size() * 8);
+  P->o_t1 = put(t1.data(), t1.size() * 8);
+  P->o_cum1 = put(cum1.data(), cum1.size() * 8);
+  P->o_t2 = put(t2.data(), t2.size() * 8);
+  P->o_cum2 = put(cum2.data(), cum2.size() * 8);
+  P->total = total;
+  AsmTables& t = P->t;
   for (int a = 0; a < 3; ++a) {
     t.un[a] = g.un[a];
     t.rl[a] = ac[a].rl;
@@ -451,41 +448,101 @@ int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr*
     t.singleton[a] = ac[a].singleton ? 1 : 0;
     t.ncls[a] = ac[a].ncls;
   }
-  t.start = reinterpret_cast<const int64_t*>(d_blob + o_start);
-  t.interior = reinterpret_cast<const int*>(d_blob + o_int);
-  t.tnnz = reinterpret_cast<const int64_t*>(d_blob + o_tnnz);
-  t.toff = reinterpret_cast<const int64_t*>(d_blob + o_toff);
-  t.tcomp = reinterpret_cast<const int4*>(d_blob + o_tcomp);
-  t.tval = reinterpret_cast<const double*>(d_blob + o_tval);
-  t.cum0 = reinterpret_cast<const int64_t*>(d_blob + o_cum0);
-  t.t1 = reinterpret_cast<const int64_t*>(d_blob + o_t1);
-  t.cum1 = reinterpret_cast<const int64_t*>(d_blob + o_cum1);
-  t.t2 = reinterpret_cast<const int64_t*>(d_blob + o_t2);
-  t.cum2 = reinterpret_cast<const int64_t*>(d_blob + o_cum2);
   t.rows = g.rows;
-  int st = SK_OK;
-  if (g.rows > 0) {
-    const unsigned grid = unsigned((g.rows + 255) / 256);
-    if (index_bits == 32)
+  return SK_OK;
+}
+
+// Device half: upload the blob, write row_ptr / col / val of m.
+int asm_launch(AsmPlan& P, sk_csr* m, cudaStream_t stream) {
+  if (m->rows == 0) {
+    const int64_t zero = 0;
+    SK_CUDA_TRY(cudaMemcpyAsync(m->row_ptr, &zero, sizeof(zero), cudaMemcpyHostToDevice, stream));
+    SK_CUDA_TRY(cudaStreamSynchronize(stream));
+    return SK_OK;
+  }
+  unsigned char* d_blob = nullptr;
+  SK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_blob), P.blob.size(), stream));
+  cudaError_t e = cudaMemcpyAsync(d_blob, P.blob.data(), P.blob.size(), cudaMemcpyHostToDevice, stream);
+  AsmTables t = P.t;
+  t.start = reinterpret_cast<const int64_t*>(d_blob + P.o_start);
+  t.interior = reinterpret_cast<const int*>(d_blob + P.o_int);
+  t.tnnz = reinterpret_cast<const int64_t*>(d_blob + P.o_tnnz);
+  t.toff = reinterpret_cast<const int64_t*>(d_blob + P.o_toff);
+  t.tcol = reinterpret_cast<const int64_t*>(d_blob + P.o_tcol);
+  t.tval = reinterpret_cast<const double*>(d_blob + P.o_tval);
+  t.cum0 = reinterpret_cast<const int64_t*>(d_blob + P.o_cum0);
+  t.t1 = reinterpret_cast<const int64_t*>(d_blob + P.o_t1);
+  t.cum1 = reinterpret_cast<const int64_t*>(d_blob + P.o_cum1);
+  t.t2 = reinterpret_cast<const int64_t*>(d_blob + P.o_t2);
+  t.cum2 = reinterpret_cast<const int64_t*>(d_blob + P.o_cum2);
+  if (e == cudaSuccess) {
+    const unsigned grid = unsigned((m->rows + 255) / 256);
+    if (m->index_bits == 32)
       assemble_kernel<int32_t><<<grid, 256, 0, stream>>>(t, m->row_ptr, static_cast<int32_t*>(m->col), m->val);
     else
       assemble_kernel<int64_t><<<grid, 256, 0, stream>>>(t, m->row_ptr, static_cast<int64_t*>(m->col), m->val);
     g_launches++;
     e = cudaGetLastError();
-    if (e != cudaSuccess) st = cuda_fail(e, "assemble_kernel");
-  } else {
-    const int64_t zero = 0;
-    e = cudaMemcpyAsync(m->row_ptr, &zero, sizeof(zero), cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) st = cuda_fail(e, "row_ptr init");
   }
   cudaFreeAsync(d_blob, stream);
-  if (st != SK_OK) {
+  if (e != cudaSuccess) return cuda_fail(e, "assemble_kernel");
+  return SK_OK;
+}
+
+}  // namespace
+
+// Free the SELL copy (rebuilt lazily by the next SpMV / CG plan).
+static void csr_drop_sell(sk_csr* m) {
+  if (!m->sell_val) return;
+  cudaDeviceSynchronize();  // no SpMV in flight may still read it
+  cudaFree(m->sell_ptr);
+  cudaFree(m->sell_len);
+  cudaFree(m->sell_val);
+  cudaFree(m->sell_col);
+  m->sell_ptr = nullptr;
+  m->sell_len = nullptr;
+  m->sell_val = nullptr;
+  m->sell_col = nullptr;
+  m->sell_entries = 0;
+}
+
+int csr_assemble(const sk_stencil* s, const GridInfo& g, int index_bits, sk_csr** out, cudaStream_t stream) {
+  if (int st = check_width(s, g)) return st;
+  if (index_bits != 32 && index_bits != 64) return fail(SK_ERR_INVALID_ARGUMENT, "index_bits must be 32 or 64");
+  if (index_bits == 32 && g.rows > int64_t(INT32_MAX)) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for int32 columns");
+  AsmPlan P;
+  if (int st = asm_plan(s, g, &P)) return st;
+  auto* m = new sk_csr;
+  m->rows = m->cols = g.rows;
+  m->nnz = P.total;
+  m->index_bits = index_bits;
+  cudaError_t e = cudaMalloc(&m->row_ptr, sizeof(int64_t) * size_t(g.rows + 1));
+  if (e == cudaSuccess && P.total > 0) e = cudaMalloc(&m->col, size_t(P.total) * (index_bits / 8));
+  if (e == cudaSuccess && P.total > 0) e = cudaMalloc(&m->val, sizeof(double) * size_t(P.total));
+  if (e != cudaSuccess) {
+    delete m;
+    return cuda_fail(e, "csr_assemble allocation");
+  }
+  if (int st = asm_launch(P, m, stream)) {
     delete m;
     return st;
   }
   *out = m;
   return SK_OK;
+}
+
+// Re-assemble into an existing matrix of the same shape (no allocation): the
+// pattern and values are rewritten; the SELL copy and every cached solver plan
+// keyed by the matrix are invalidated (new uid).
+int csr_assemble_into(const sk_stencil* s, const GridInfo& g, sk_csr* m, cudaStream_t stream) {
+  if (int st = check_width(s, g)) return st;
+  AsmPlan P;
+  if (int st = asm_plan(s, g, &P)) return st;
+  if (m->rows != g.rows || m->cols != g.rows || m->nnz != P.total)
+    return fail(SK_ERR_SHAPE_MISMATCH, "matrix shape or nonzero count differs from the assembled operator");
+  csr_drop_sell(m);
+  m->uid = sk_next_csr_uid();
+  return asm_launch(P, m, stream);
 }
 
 __global__ void narrow_cols(int64_t n, const int64_t* __restrict__ in, int32_t* __restrict__ out) {
@@ -502,6 +559,13 @@ __global__ void widen_cols(int64_t n, const int32_t* __restrict__ in, int64_t* _
 using namespace sk;
 
 extern "C" {
+
+int sk_csr_assemble_into(const sk_stencil* s, const sk_grid_desc* gd, sk_csr* m, void* stream) {
+  if (!s || !m) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil or matrix");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  return csr_assemble_into(s, g, m, as_stream(stream));
+}
 
 int sk_csr_assemble(const sk_stencil* s, const sk_grid_desc* gd, int index_bits, sk_csr** out, void* stream) {
   if (!s || !out) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil or output");

@@ -170,6 +170,14 @@ def assemble(s, g: GridSpec, index_bits: int = 64, stream=None) -> CsrMatrix:
     return CsrMatrix(h.value)
 
 
+def assemble_into(s, g: GridSpec, m: "CsrMatrix", stream=None) -> "CsrMatrix":
+    """Re-assemble the operator into an existing matrix of the same shape (sk_csr_assemble_into)."""
+    ds = as_device_stencil(s)
+    d = g.desc()
+    check(ds.lib.sk_csr_assemble_into(ds.handle, C.byref(d), m.handle, stream))
+    return m
+
+
 def csr_matmul(b: CsrMatrix, a: CsrMatrix, stream=None) -> CsrMatrix:
     """b * a on the device (linalg.cpp:253-283), bit-identical values."""
     if b.cols != a.rows:

@@ -313,6 +313,31 @@ def test_assembly_large_sampled_rows(orc):
     assert np.all(np.diff(rp) > 0)
 
 
+@pytest.mark.parametrize("bits", [64, 32])
+def test_assemble_into_reuses_the_matrix(orc, bits):
+    # re-assembly into an existing matrix (new h -> new weights, same pattern)
+    # is bit-identical to a fresh assembly; the cached SELL copy / CG plan of
+    # the matrix follow the new values; a shape change is rejected
+    from paper_2205_03354_b200.grid import assemble_into
+
+    s = bilaplacian(3, 4)
+    g1 = make_grid(3, 21, 1.0 / 20, BoundaryKind.clamped)
+    g2 = make_grid(3, 21, 1.0 / 7, BoundaryKind.clamped)
+    m = assemble(s, g1, index_bits=bits)
+    x = uniform(5, m.rows)
+    y1 = apply(m, x)  # builds the SELL copy
+    assemble_into(s, g2, m)
+    rp, ci, v = m.to_host()
+    orp, oci, ov = orc.assemble(s, g2)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci) and np.array_equal(v, ov)
+    y2 = apply(m, x)
+    assert np.array_equal(y2, apply(assemble(s, g2, index_bits=bits), x))
+    assert not np.array_equal(y1, y2)
+    with pytest.raises(StencilkitError) as e:
+        assemble_into(s, make_grid(3, 19, 1.0 / 18, BoundaryKind.clamped), m)
+    assert e.value.code == Errc.shape_mismatch
+
+
 def test_assembly_errors():
     with pytest.raises(StencilkitError) as e:
         assemble(bilaplacian(2), make_periodic_grid(2, 4, 1.0))

@@ -108,3 +108,25 @@ def test_refined_solve_config5_small(orc):
     e0, e1 = np.abs(x0 - u).max(), np.abs(x - u).max()
     assert abs(e1 - e0) <= 1e-3 * e0  # discretisation error dominates at N = 32
     assert np.linalg.norm(x - x0) <= 1e-8 * np.linalg.norm(x0)
+
+
+@pytest.mark.gpu
+def test_config5_fourth_order_at_256(orc):
+    """Config 5 at its own sizes (128^3 and 256^3 intervals): with the exact-operator
+    refinement the pairwise observed order (experiments.cpp:128-141) is ~4 and the
+    256^3 error is the 4th-order prediction (128^3 error / 16)."""
+    import math
+
+    s = DeviceStencil(bilaplacian(3, 4))
+    o = SolveOptions(rel_tol=1e-10, accept_recurrence=True, check_every=256)
+    errs = {}
+    for N in (128, 256):
+        g = make_grid(3, N + 1, 1.0 / N, BoundaryKind.clamped)
+        f, u = orc.biharmonic_clamped(3, N)
+        rep = RefineReport()
+        x = cg_solve_stencil_refined(s, g, f, o, 1e-6, 4, rep)
+        assert rep.last_correction_rel <= 1e-13
+        errs[N] = float(np.abs(x - u).max())
+    order = math.log(errs[128] / errs[256]) / math.log(2.0)
+    assert order >= 3.9, (errs, order)
+    assert errs[256] <= 1.05 * errs[128] / 16
