@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(CoopTile::THREADS, 4) k_cg2d_coop(const Coop2D
     }
     acc = block_sum<T>(acc, red);
     if (threadIdx.x == 0) c.part_a[blockIdx.x] = acc;
+    sk_jitter(40);
     grid.sync();
     pq = block_broadcast_sum<T>(c.part_a, G, red, &bcast);
     if (pq <= 0) {  // linalg.cpp:50-51
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(CoopTile::THREADS, 4) k_cg2d_coop(const Coop2D
     }
     acc = block_sum<T>(acc, red);
     if (threadIdx.x == 0) c.part_b[blockIdx.x] = acc;
+    sk_jitter(40);
     grid.sync();
     const double rho_next = block_broadcast_sum<T>(c.part_b, G, red, &bcast);
     beta = rho_next / rho;

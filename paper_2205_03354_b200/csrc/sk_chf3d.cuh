@@ -247,10 +247,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       const int s_iss = s_load;  // LD 1: the stage refilled in this step (plane k-3's)
       if constexpr (LD == 0) {
         cp_async_wait_group<S - 4>();
+        sk_jitter(14);
         __syncthreads();
         lc.issue_next(ring, s_load, a);
       } else {
         mbar_wait(&bars[s_k], ph);  // plane k landed
+        sk_jitter(10);
       }
       s_load = s_load + 1 == S ? 0 : s_load + 1;
       const int s_k1 = s_k == 0 ? S - 1 : s_k - 1;   // stage of plane k-1
@@ -278,7 +280,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       };
       if constexpr (DO_OUT && V == 0 && LD == 0) out_neighbours();
       if constexpr (LD == 1 && !kLateWait) {  // all warps past step t-1: the mu slot written below is free
+        sk_jitter(11);
+#ifndef SK_RACE_SELFTEST_DROP_STEP_WAIT  // tools/race_jitter.py: proves the detector sees a missing wait
         if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
+#endif
       }
       if constexpr (DO_MU && V == 1) {
 #pragma unroll
@@ -322,12 +327,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       };
       if constexpr (LD == 1) {
         border_mu();
+        sk_jitter(12);
         __syncwarp();
         if (lane == 0) mbar_arrive(&stepbar[sb]);  // this warp is done with step t's stages and mu slot
         if constexpr (kLateWait) {  // 4 mu slots: the slot written above was last read in step t-3
           if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
         }
         if (threadIdx.x == 0) {  // stage of plane k-3 is free (last read at step t-1)
+          sk_jitter(13);
           fence_proxy_async_smem();
           tc.issue_next(ring, bars, s_iss, a, &tmap);
         }

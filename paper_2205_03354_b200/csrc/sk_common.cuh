@@ -54,6 +54,25 @@ double pow_int(double base, int exp);                  // grid.cpp:10-15, bit-id
 constexpr int kNumSMs = 148;
 
 // ---- device helpers --------------------------------------------------------
+// Race amplification (test builds only, -DSK_RACE_JITTER, tools/race_jitter.py):
+// a pseudo-random sleep of up to ~1 us for one thread in four at every
+// synchronisation point of the kernels, so a missing barrier / fence /
+// mbarrier wait shows up as a changed result instead of hiding behind lucky
+// timing. Compiles to nothing in the product build.
+#ifdef SK_RACE_JITTER
+__device__ __forceinline__ void sk_jitter(unsigned site) {
+  unsigned t;
+  asm volatile("mov.u32 %0, %%clock;" : "=r"(t));
+  unsigned h = t ^ (threadIdx.x * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu) ^ (site * 0xC2B2AE35u);
+  h ^= h >> 13;
+  h *= 0x5BD1E995u;
+  h ^= h >> 15;
+  if ((h & 3u) == 0u) __nanosleep((h >> 16) & 1023u);
+}
+#else
+__device__ __forceinline__ void sk_jitter(unsigned) {}
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -154,6 +173,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   static_assert(THREADS % 32 == 0 && THREADS <= 1024, "block size");
   v = warp_sum(v);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  sk_jitter(1);
   __syncthreads();  // sh may be reused back to back
   if (lane == 0) sh[warp] = v;
   __syncthreads();
@@ -169,6 +189,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // so the two-level reduction is deterministic for a given grid size.
 __device__ __forceinline__ bool last_block(unsigned* counter, unsigned nblocks) {
   __shared__ bool is_last;
+  sk_jitter(2);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

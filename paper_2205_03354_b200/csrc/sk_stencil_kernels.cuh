@@ -163,6 +163,7 @@ __device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a,
       cp_async16(tile + r * T::PITCH + c, a.u + gy * a.nx + gx);
     }
     cp_async_wait_all();
+    sk_jitter(30);
     __syncthreads();
   } else if (inner) {  // 8-byte cp.async (rows need not be 16-byte aligned)
     const int64_t base = (y0 - R) * a.nx + (x0 - R);
@@ -171,6 +172,7 @@ __device__ __forceinline__ void load_tile_2d(double* tile, const Apply2DArgs& a,
       cp_async8(tile + i, a.u + base + r * a.nx + c);
     }
     cp_async_wait_all();
+    sk_jitter(30);
     __syncthreads();
   } else {
     for (int i = tid; i < T::ROWS * T::PITCH; i += T::THREADS) {  // any boundary kind

@@ -538,6 +538,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
         const int p = pb + st;
         if (p < np) {
           cp_async_wait_group<S - 2>();  // this thread's copies of the plane have landed
+          sk_jitter(20);
           __syncthreads();               // ... everyone's, and the previous plane is fully consumed
           lc.issue_next(ring, s_load, a);
           s_load = s_load + 1 == S ? 0 : s_load + 1;
