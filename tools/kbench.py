@@ -47,10 +47,14 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--steps", type=int, default=2, help="CH steps per timed call (>= 100: graph chunks)")
     ap.add_argument("--lib", default=None, help="alternative build (tools/ab_build.py)")
+    ap.add_argument("--opt", action="append", default=[], help="sk_set_option name=value (repeatable)")
     args = ap.parse_args()
     if args.lib:
         _lib.load(Path(args.lib))
     lib = _lib.ensure_device(0)
+    for o in args.opt:
+        k, v = o.split("=")
+        _lib.set_option(k, int(v))
     rng = np.random.default_rng(0)
     case = args.case
     if case.startswith("ch"):
