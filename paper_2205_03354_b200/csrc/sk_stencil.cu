@@ -17,7 +17,7 @@
 #include "sk_internal.hpp"
 #include "sk_stencil_kernels.cuh"
 #include "sk_stream3d.cuh"
-#include "sk_fac3d.cuh"
+#include "sk_fac73.cuh"
 
 sk_stencil::~sk_stencil() {
   if (rep_exec) cudaGraphExecDestroy(rep_exec);
@@ -282,24 +282,23 @@ static bool is_l4l4(const sk_stencil* s) {
   return true;
 }
 
-// Factored 73-point apply (sk_fac3d.cuh): L4 weights (centre 3 * -30/12,
-// axis +-1: 16/12, axis +-2: -1/12, generators.cpp:98) scaled by h^-2 per pass.
+// Factored 73-point apply (sk_fac73.cuh): L4 weights (centre 3 * -30/12,
+// axis +-1: 16/12, axis +-2: -1/12, generators.cpp:98) scaled by h^-2 per
+// pass. 16-byte periodic path only (whole-tile halos, even nx); returns
+// kApplyPqUnsupported when the grid needs the literal kernel instead.
 static int launch_fac73(Args3D a, double h_m2, cudaStream_t stream) {
-  using C = CfgFac73;
-  using SM = FacSmem<C>;
+  using C = CfgF2;
+  using SM = F2Smem<C>;
+  if (!a.bulk_ok || a.nx < C::TX + 2 * C::R || a.ny < C::TY + 2 * C::R) return kApplyPqUnsupported;
   const L4W lw{(3.0 * (-30.0 / 12.0)) * h_m2, (16.0 / 12.0) * h_m2, (-1.0 / 12.0) * h_m2};
-  auto bulk = fac73_kernel<C, false>;
-  auto fallback = fac73_kernel<C, true>;
-  static int once = set_smem(bulk, SM::BYTES) != SK_OK ? SK_ERR_CUDA : set_smem(fallback, SM::BYTES_FB);
+  auto kern = fac73v2_kernel<C>;
+  static int once = set_smem(kern, SM::BYTES);
   if (once != SK_OK) return once;
   a.zrot = 1;
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/false);
-  if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
-  if (a.bulk_ok)
-    bulk<<<unsigned(grid), C::THREADS, SM::BYTES, stream>>>(a, lw);
-  else
-    fallback<<<unsigned(grid), C::THREADS, SM::BYTES_FB, stream>>>(a, lw);
-  SK_LAUNCH_CHECK("fac73_kernel");
+  if (grid == 0 || !a.bulk_ok) return kApplyPqUnsupported;
+  kern<<<unsigned(grid), C::THREADS, SM::BYTES, stream>>>(a, lw);
+  SK_LAUNCH_CHECK("fac73v2_kernel");
   return SK_OK;
 }
 
@@ -339,7 +338,10 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     a.bulk_ok = per && (a.nx % 2 == 0) && a.nx >= C3R4::TX + 2 * C3R4::R && a.ny >= C3R4::TY + 2 * C3R4::R &&
                 aligned16(u) && aligned16(v);
     if (per && is_l4l4(s)) {  // B = compose(L4, L4) on a periodic grid: two fused L4 passes possible
-      if (option(SK_OPT_APPLY73_FACTORED)) return launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
+      if (option(SK_OPT_APPLY73_FACTORED)) {
+        const int st = launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
+        if (st != kApplyPqUnsupported) return st;
+      }
     }
     if (a.bulk_ok && a.nx >= Cfg3R4P::TX + 2 * Cfg3R4P::R && a.ny >= Cfg3R4P::TY + 2 * Cfg3R4P::R)
       return launch_3d<Mode::Apply, Cfg3R4P>(a, stream);

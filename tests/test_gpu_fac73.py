@@ -1,4 +1,4 @@
-"""Factored 73-point apply (sk_fac3d.cuh, opt-in SK_F73=1): B = compose(L4, L4) on periodic grids
+"""Factored 73-point apply (sk_fac73.cuh, default on periodic 16-byte grids; SK_OPT_APPLY73_FACTORED): B = compose(L4, L4)
 as two fused fourth-order Laplacian passes.
 
 The operator is the reference's composed stencil (stencil.cpp:75-87 applied to
