@@ -651,7 +651,15 @@ def main() -> int:
     peak, peak_kind = peak_hbm()
     bytes_step = 16.0 * r["points"]
     achieved = bytes_step / (ms_step * 1e-3) / 1e9
-    kernel = "chf3d_kernel" if dim == 3 else "stencil2d_kernel<CahnHilliard>"
+    if dim == 3 and args.steps >= 2:  # one chunk graph: first step (cp.async) + TMA steps on ghost-padded buffers
+        kernel = "chf3d_kernel<Cfg3<2,64,16,2,2,7,2>,0,1,1,0> (TMA, ghost-padded mid-chunk step)"
+        ncu_key = "chf3d_kernel TMA mid-chunk (r2)"
+        launch_mix = {"first (cp.async, plain -> padded)": 1, "mid (TMA, padded -> padded)": max(args.steps - 2, 0),
+                      "last (TMA, padded -> plain)": 1}
+    elif dim == 3:
+        kernel, ncu_key, launch_mix = "chf3d_kernel (cp.async, plain field)", "chf3d_kernel (r1)", {"single": 1}
+    else:
+        kernel, ncu_key, launch_mix = "stencil2d_kernel<CahnHilliard>", "stencil2d_kernel_ch", {"2D step": args.steps}
     line = {
         "metric": "CH steps/s",
         "value": value,
@@ -671,9 +679,11 @@ def main() -> int:
         "clocks": r["clocks"],
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy read+write)", "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(kernel),
-                     "traffic_steady_state": ncu_traffic(kernel, steady=True),
-                     "algorithmic_bytes_per_launch": bytes_step},
+                     "frac": achieved / peak, "traffic": ncu_traffic(ncu_key),
+                     "traffic_source": f"profiles/ncu_summary.json[{ncu_key!r}] (dram read + write per launch)",
+                     "algorithmic_bytes_per_launch": bytes_step, "launch_mix": launch_mix,
+                     "achieved_note": "algorithmic bytes / CUDA-event step time averaged over the timed K-step "
+                                      "call (all launch kinds of the chunk)"},
     }
     if "e2e_s" in r:
         line["e2e"] = {"value": args.steps / r["e2e_s"] * d.world, "unit": "steps/s",
