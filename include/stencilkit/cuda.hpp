@@ -22,6 +22,7 @@
 
 #include <sk_cuda.h>
 
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <span>
@@ -60,19 +61,36 @@ inline sk_grid_desc grid_desc(const GridSpec& g, bool clamped = false) {
   return d;
 }
 
+/// q - hi exactly, rounded once (hi = q.to_double()): the exact-weight
+/// correction of sk_stencil_create_exact. 0 when hi is outside the range a
+/// long-denominator Rational represents exactly (|hi| < 2^-10: not a composed
+/// FD weight of the configs).
+inline double rational_residue(const Rational& q, double hi) {
+  if (hi == 0.0) return q.to_double();
+  int e = 0;
+  const double f = std::frexp(hi, &e);  // hi = f 2^e, f in [0.5, 1)
+  const long m = static_cast<long>(std::ldexp(f, 53));
+  const int sh = 53 - e;
+  if (sh < 0 || sh > 62) return 0.0;
+  return (q - Rational(m, 1L << sh)).to_double();
+}
+
 /// A composed stencil uploaded for the device: offsets in the Stencil's map
-/// order, coefficients as Rational::to_double() (rational.hpp:32).
+/// order, coefficients as Rational::to_double() (rational.hpp:32), plus their
+/// exact-weight corrections (used only by the refined residual / solver).
 class DeviceStencil {
  public:
   explicit DeviceStencil(const Stencil& s) {
     std::vector<int32_t> off;
-    std::vector<double> coeff;
+    std::vector<double> coeff, lo;
     for (const auto& [o, c] : s.entries()) {
       off.insert(off.end(), o.begin(), o.end());
       coeff.push_back(c.to_double());
+      lo.push_back(rational_residue(c, coeff.back()));
     }
     sk_stencil* h = nullptr;
-    check(sk_stencil_create(s.dim(), static_cast<int>(coeff.size()), off.data(), coeff.data(), s.h_power(), &h));
+    check(sk_stencil_create_exact(s.dim(), static_cast<int>(coeff.size()), off.data(), coeff.data(), lo.data(),
+                                  s.h_power(), &h));
     h_.reset(h);
   }
   sk_stencil* get() const { return h_.get(); }
@@ -230,6 +248,31 @@ inline std::vector<double> composed_apply(const Stencil& s, const GridSpec& g, s
   std::vector<double> v(u.size());
   check(sk_composed_apply_host(ds.get(), &d, u.data(), v.data()));
   return v;
+}
+
+/// Matrix-free CG on the composed operator, then iterative refinement against
+/// the EXACT rational operator (double-double residual): the solution of the
+/// exact discrete system instead of the fp64-weight matrix (BVP configs 2/5;
+/// experiments.cpp:99-143 is the driver it serves). opts.rel_tol is the first
+/// solve's recurrence tolerance (the fp64 true-residual floor makes the
+/// reference's acceptance unattainable at config sizes).
+inline std::vector<double> cg_solve_refined(const Stencil& s, const GridSpec& g, std::span<const double> b,
+                                            const SolveOptions& opts = {}, bool clamped = false,
+                                            double inner_rel_tol = 1e-6, int max_refinements = 4,
+                                            sk_refine_report* report = nullptr) {
+  const DeviceStencil ds(s);
+  const sk_grid_desc d = grid_desc(g, clamped);
+  if (static_cast<int64_t>(b.size()) != g.unknown_count())
+    throw Error(Errc::shape_mismatch, "rhs length does not match the grid");
+  const sk_solve_options o{opts.rel_tol, opts.max_iter, opts.deflate_mean ? 1 : 0, 0, 1, 0};
+  const DeviceField db(b);
+  DeviceField dx(b.size());
+  check(sk_cg_solve_stencil_refined(ds.get(), &d, db.data(), dx.data(), &o, inner_rel_tol, max_refinements, report,
+                                    nullptr));
+  std::vector<double> x(b.size());
+  dx.download(x);
+  check(sk_stream_sync(nullptr));
+  return x;
 }
 
 inline sk_ch_params ch_params(const CahnHilliardParams& p, int formulation = SK_CH_FACTORED) {

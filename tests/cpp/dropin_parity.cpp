@@ -195,6 +195,28 @@ int main() {
     const CsrMatrix r = csr_matmul(b, a), c = cuda::csr_matmul(b, a);
     EXPECT(r.row_ptr == c.row_ptr && r.col_idx == c.col_idx && r.values == c.values, "csr_matmul bit-identical");
   }
+  {  // exact-operator refinement (configs 2 / 5): the 73-point composition's Rational
+     // coefficients reach the device as double + exact residue; the refined
+     // solve agrees with the plain one where the weight rounding is negligible
+    const Stencil bih = compose(laplacian(3, 4), laplacian(3, 4));
+    const int N = 16;
+    const GridSpec g = ss_grid(3, N);
+    std::vector<double> b(static_cast<size_t>(g.unknown_count()));
+    for (size_t i = 0; i < b.size(); ++i) b[i] = std::sin(0.01 * double(i)) + 1.0;
+    sk_refine_report rep{};
+    const std::vector<double> xr = cuda::cg_solve_refined(bih, g, b, SolveOptions{1e-10, 0, false}, true, 1e-6, 4, &rep);
+    const std::vector<double> x0 = cuda::cg_solve(cuda::DeviceCsr(bih, g, true), b, SolveOptions{1e-9, 0, false});
+    double d = 0, nn = 0;
+    for (size_t i = 0; i < b.size(); ++i) {
+      d += (xr[i] - x0[i]) * (xr[i] - x0[i]);
+      nn += x0[i] * x0[i];
+    }
+    EXPECT(rep.refinements >= 1 && rep.last_correction_rel <= 1e-13, "refinement converged to fp64 resolution");
+    EXPECT(std::sqrt(d) <= 1e-7 * std::sqrt(nn), "refined solve agrees with cg_solve (clamped 73-point, 15^3)");
+    EXPECT(cuda::rational_residue(Rational(1607, 24), Rational(1607, 24).to_double()) != 0.0 &&
+               cuda::rational_residue(Rational(20), 20.0) == 0.0,
+           "exact residues of non-dyadic / integer weights");
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }
