@@ -24,10 +24,12 @@
 //            -> output plane k-2: L mu the same way (shuffles, mu ring rows,
 //               registers) + c of plane k-2 (register); 128-bit stores.
 // Shared-memory traffic per point is ~1/2 of a window-load design (the
-// kernel was bound by shared wavefronts: ncu, profiles/). One __syncthreads
-// per plane orders everything (mu slot of plane k-1 is written at step k and
-// read at step k+1; c stage k-3 is refilled at step k). The step loop is
-// unrolled by 3 so every register / slot role is static.
+// kernel was bound by shared wavefronts: ncu, profiles/). Stages complete on
+// FULL mbarriers (TMA bytes, or every thread's cp.async arrivals); a
+// split-phase step barrier orders the rest (mu slot of plane k-1 is written
+// at step k and read at step k+1; c stage k-3 is refilled at step k; see the
+// comment at `stepbar`). The step loop is unrolled by 3 so every register /
+// slot role is static.
 #pragma once
 
 #include <cuda.h>
@@ -87,7 +89,8 @@ struct ChfSmem {
   static constexpr int BORDER_ROWS = 2 * (C::TX + 2);                     // mu rows -1 and TY, x in [-1, TX]
   static constexpr int ROWS_PER_WARP = (BORDER_ROWS + WARPS - 1) / WARPS;  // + 4 side points per warp
   static_assert(ROWS_PER_WARP + 4 <= 32, "border points per warp");
-  static_assert(!LD || (STAGE_BYTES % 128 == 0 && (C::STAGES + 3) * 8 <= 128), "TMA stage alignment + step barriers");
+  static_assert(!LD || STAGE_BYTES % 128 == 0, "TMA stage alignment");
+  static_assert((C::STAGES + 3) * 8 <= (LD ? 128 : C::RING_OFS), "full + step barriers before the ring");
   static_assert(!LD || (C::ROWS % kTmaSplit == 0 && (C::ROWS / kTmaSplit) * P * 8 % 128 == 0), "TMA box split");
 };
 
@@ -153,22 +156,32 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   // programmatic dependent launch: wait for the previous step (which wrote
   // our input) before the first load; the next step is released at the end
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // FULL barrier per stage: TMA (LD 1) completes its bytes on it; with
+  // cp.async (LD 0) every thread's copies arrive on it (arrive.noinc), so the
+  // data needs no CTA barrier either. Then three step barriers (below).
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&bars[i], LD ? 1 : C::THREADS);
+    for (int i = 0; i < 3; ++i) mbar_init(&bars[S + i], C::THREADS / 32);  // step barriers: one arrival per warp
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // LD 0: issue the next plane into stage `st` (this thread's copies) and arm its FULL barrier
+  auto cp_issue = [&](int st) {
+    if (lc.u < lc.uend) {
+      lc.issue_next(ring, st, a);
+      cp_async_arrive_noinc(&bars[st]);
+    }
+  };
   if constexpr (LD == 0) {
     lc.u = ubeg;
     lc.uend = uend;
     if (ubeg < uend) lc.start(a, ring);
 #pragma unroll 1
     for (int k = 0; k < S - 3; ++k) {
-      lc.issue_next(ring, s_load, a);
+      cp_issue(s_load);
       s_load = s_load + 1 == S ? 0 : s_load + 1;
     }
   } else {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
-      for (int i = 0; i < 3; ++i) mbar_init(&bars[S + i], C::THREADS / 32);  // step barriers: one arrival per warp
-      fence_mbar_init();
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
       tc.u = ubeg;
       tc.uend = uend;
@@ -244,16 +257,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       constexpr int M1 = (K + 2) % 3, M2 = (K + 1) % 3, M3 = K;  // mu of planes k-1, k-2, k-3
       (void)M2;
       (void)M3;
-      const int s_iss = s_load;  // LD 1: the stage refilled in this step (plane k-3's)
-      if constexpr (LD == 0) {
-        cp_async_wait_group<S - 4>();
-        sk_jitter(14);
-        __syncthreads();
-        lc.issue_next(ring, s_load, a);
-      } else {
-        mbar_wait(&bars[s_k], ph);  // plane k landed
-        sk_jitter(10);
-      }
+      const int s_iss = s_load;  // the stage refilled in this step (plane k-3's)
+      mbar_wait(&bars[s_k], ph);  // plane k landed
+      sk_jitter(10);
       s_load = s_load + 1 == S ? 0 : s_load + 1;
       const int s_k1 = s_k == 0 ? S - 1 : s_k - 1;   // stage of plane k-1
       const int s_k2 = s_k1 == 0 ? S - 1 : s_k1 - 1;  // stage of plane k-2
@@ -278,13 +284,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         oup = ld2(mb - MP);
         odn = ld2(mb + 2 * MP);
       };
-      if constexpr (DO_OUT && V == 0 && LD == 0) out_neighbours();
-      if constexpr (LD == 1 && !kLateWait) {  // all warps past step t-1: the mu slot written below is free
+      if constexpr (!kLateWait) {  // all warps past step t-1: the mu slot written below is free
         sk_jitter(11);
 #ifndef SK_RACE_SELFTEST_DROP_STEP_WAIT  // tools/race_jitter.py: proves the detector sees a missing wait
         if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
 #endif
       }
+      if constexpr (LD == 0) cp_issue(s_iss);  // stage of plane k-3 is free (last read at step t-1)
       if constexpr (DO_MU && V == 1) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) M[M1][i] = Cz[C1][i];
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           }
         }
       };
-      if constexpr (LD == 1) {
+      {
         border_mu();
         sk_jitter(12);
         __syncwarp();
@@ -333,10 +339,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         if constexpr (kLateWait) {  // 4 mu slots: the slot written above was last read in step t-3
           if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
         }
-        if (threadIdx.x == 0) {  // stage of plane k-3 is free (last read at step t-1)
-          sk_jitter(13);
-          fence_proxy_async_smem();
-          tc.issue_next(ring, bars, s_iss, a, &tmap);
+        if constexpr (LD == 1) {
+          if (threadIdx.x == 0) {  // stage of plane k-3 is free (last read at step t-1)
+            sk_jitter(13);
+            fence_proxy_async_smem();
+            tc.issue_next(ring, bars, s_iss, a, &tmap);
+          }
         }
         if constexpr (DO_OUT && V == 0) out_neighbours();
         started = true;
@@ -391,7 +399,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
         }
         outp += opp;
       }
-      if constexpr (LD == 0) border_mu();
       if (++s_k == S) {
         s_k = 0;
         ph ^= 1u;

@@ -66,10 +66,6 @@ struct F2Smem {
   static_assert(WP % 2 == 0, "16-byte w rows");
 };
 
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // L4 at a pair of points (x, x+1) of one row: centre pair c, left pair
 // (x-2, x-1), right pair (x+2, x+3), the pairs of rows y-1, y+1, y-2, y+2 and
 // the z-neighbour pairs; s_d = ((x +- d) + (y +- d)) + (z +- d).
