@@ -165,7 +165,8 @@ enum sk_option {
   SK_OPT_CG_PQ = 5,            /* 3D radius-2 matrix-free CG: p.q reduced in the apply epilogue: 1 */
   SK_OPT_IMEX_MATRIX_FREE = 6, /* IMEX implicit operator applied matrix-free (0: CSR SpMV): 1 */
   SK_OPT_APPLY73_FACTORED = 7, /* periodic 73-point apply as L4(L4 u) (0: literal 73 weights): 1 */
-  SK_OPT_COUNT = 8
+  SK_OPT_CG_PADDED = 8,        /* radius-4 matrix-free CG off periodic grids: ghost-padded p (16-byte loads): 1 */
+  SK_OPT_COUNT = 9
 };
 int sk_set_option(int option, int value);
 int sk_get_option(int option, int* value);

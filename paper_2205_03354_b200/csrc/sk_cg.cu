@@ -129,6 +129,130 @@ __global__ void k3_xpby(int64_t n, const double* __restrict__ r, double* __restr
     p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
+// Ghost-padded copy of p for the radius-4 matrix-free apply on non-periodic
+// grids (launch_apply_padded): every interior point is written at its padded
+// position and at each of its ghost images (assemble's boundary handling,
+// grid.cpp:104-122: even reflection about the boundary point for clamped,
+// odd for simply supported, wrap for periodic axes); the boundary points
+// (padded -1 and un) stay 0 from the initial memset. Per axis a point x has
+// the image -x-2 when x < R and 2un-x when x >= un-R (periodic: x+un / x-un).
+struct PadLayout {
+  int pad = 0;         // frame width (>= R + 1, even)
+  int64_t px = 0, py = 0, plane = 0;  // row and plane pitch (elements)
+  int64_t un[3] = {0, 0, 0};
+  int bc[3] = {0, 0, 0};
+  int R = 4;
+  __host__ __device__ int64_t at(int64_t x, int64_t y, int64_t z) const {
+    return (z + pad) * plane + (y + pad) * px + (x + pad);
+  }
+};
+
+__device__ __forceinline__ int pad_images(const PadLayout& L, int a, int64_t x, int64_t* pos, double* sgn) {
+  pos[0] = x;
+  sgn[0] = 1.0;
+  int n = 1;
+  const int64_t un = L.un[a];
+  if (L.bc[a] == SK_BC_PERIODIC) {
+    if (x < L.R) { pos[n] = x + un; sgn[n++] = 1.0; }
+    if (x >= un - L.R) { pos[n] = x - un; sgn[n++] = 1.0; }
+  } else {
+    const double s = L.bc[a] == SK_BC_SIMPLY_SUPPORTED ? -1.0 : 1.0;
+    if (x < L.R) { pos[n] = -x - 2; sgn[n++] = s; }
+    if (x >= un - L.R) { pos[n] = 2 * un - x; sgn[n++] = s; }
+  }
+  return n;
+}
+
+// one interior point (x, y, z) with value v: its padded position and images
+__device__ __forceinline__ void pad_store(const PadLayout& L, double* __restrict__ pp, int64_t x, int64_t y,
+                                          int64_t z, bool row_edge, double v) {
+  if (!row_edge && x >= L.R && x < L.un[0] - L.R) {
+    pp[L.at(x, y, z)] = v;
+    return;
+  }
+  int64_t px[3], py[3], pz[3];
+  double sx[3], sy[3], sz[3];
+  const int nx = pad_images(L, 0, x, px, sx), ny = pad_images(L, 1, y, py, sy), nz = pad_images(L, 2, z, pz, sz);
+  for (int c = 0; c < nz; ++c)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a) pp[L.at(px[a], py[b], pz[c])] = (sx[a] * sy[b] * sz[c]) * v;
+}
+
+// Row-mapped launches (block = one x-row of the interior, no per-element
+// division): grid-stride over rows, threads over x.
+__device__ __forceinline__ bool pad_row(const PadLayout& L, int64_t row, int64_t& y, int64_t& z) {
+  z = row / L.un[1];
+  y = row - z * L.un[1];
+  return y < L.R || z < L.R || y >= L.un[1] - L.R || z >= L.un[2] - L.R;
+}
+
+// Warp per interior x-row (grid-stride over rows), 8 points per lane with
+// all loads issued before the stores: the row's padded position and images.
+constexpr int kPadPts = 8;
+
+__global__ void __launch_bounds__(256) k_pad_fill(const double* __restrict__ p, double* __restrict__ pp,
+                                                  const PadLayout L) {
+  const int64_t rows = L.un[1] * L.un[2];
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  for (int64_t row = int64_t(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32; row < rows; row += warps) {
+    int64_t y, z;
+    const bool edge = pad_row(L, row, y, z);
+    const double* pr = p + row * L.un[0];
+    for (int64_t x0 = 0; x0 < L.un[0]; x0 += 32 * kPadPts) {
+      double v[kPadPts];
+#pragma unroll
+      for (int j = 0; j < kPadPts; ++j) {
+        const int64_t x = x0 + lane + 32 * j;
+        v[j] = x < L.un[0] ? pr[x] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kPadPts; ++j) {
+        const int64_t x = x0 + lane + 32 * j;
+        if (x < L.un[0]) pad_store(L, pp, x, y, z, edge, v[j]);
+      }
+    }
+  }
+}
+
+// K3 for the padded operator: p = r + beta p (bit-exact xpby) into p and its padded copy
+template <bool COND>
+__global__ void __launch_bounds__(256) k3_xpby_pad(const double* __restrict__ r, double* __restrict__ p,
+                                                   double* __restrict__ pp, const PadLayout L, const CgState* st,
+                                                   cudaGraphConditionalHandle cond) {
+  if constexpr (COND) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, st->status == kRunning ? 1u : 0u);
+  }
+  if (st->status != kRunning) return;
+  const double beta = st->beta;
+  const int64_t rows = L.un[1] * L.un[2];
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  for (int64_t row = int64_t(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32; row < rows; row += warps) {
+    int64_t y, z;
+    const bool edge = pad_row(L, row, y, z);
+    const int64_t base = row * L.un[0];
+    for (int64_t x0 = 0; x0 < L.un[0]; x0 += 32 * kPadPts) {
+      double rv[kPadPts], pv[kPadPts];
+#pragma unroll
+      for (int j = 0; j < kPadPts; ++j) {
+        const int64_t x = x0 + lane + 32 * j;
+        rv[j] = x < L.un[0] ? r[base + x] : 0.0;
+        pv[j] = x < L.un[0] ? p[base + x] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kPadPts; ++j) {
+        const int64_t x = x0 + lane + 32 * j;
+        if (x < L.un[0]) {
+          const double pi = __dadd_rn(rv[j], __dmul_rn(beta, pv[j]));
+          p[base + x] = pi;
+          pad_store(L, pp, x, y, z, edge, pi);
+        }
+      }
+    }
+  }
+}
+
 // q = M x ; out = sum (b - q)^2   (linalg.cpp:33-39, :59-61)
 template <class IDX>
 __global__ void __launch_bounds__(kT) k_true_residual(int64_t n, const int64_t* __restrict__ rp,
@@ -368,11 +492,29 @@ struct CgPlan {
   const double* graph_x = nullptr;
   bool device_loop = false;  // exec = while(status == running) { iteration } on the device
   bool pq_fused = false;     // 3D streaming stencil: the apply reduces p.q itself
+  // padded: radius-4 3D stencil on a non-periodic grid; K3 also writes a
+  // ghost-padded copy of p (ppad, layout pl) and the apply reads it with the
+  // 16-byte loader instead of the 8-byte boundary-map loader (config 5,
+  // 255^3: apply 215 -> 130 us, iteration 455 -> 415 us; p.q stays a separate
+  // pass: in the apply's epilogue it measured 511 us per iteration)
+  bool padded = false;
+  PadLayout pl;
+  double* ppad = nullptr;
   int kernels_per_iteration() const { return fused2d ? 2 : ((op.m || pq_fused) ? 3 : 4); }
 
   ~CgPlan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (ws) cudaFree(ws);
+    if (ppad) cudaFree(ppad);
+  }
+  // warp per row, 8 warps per block, 8 blocks per SM resident
+  unsigned pad_grid() const { return unsigned(std::min<int64_t>((pl.un[1] * pl.un[2] + 7) / 8, int64_t(kNumSMs) * 8)); }
+  // after p was set outside the iteration (x0 = 0 start, restart)
+  int refresh_pad(cudaStream_t stream) {
+    if (!padded) return SK_OK;
+    k_pad_fill<<<pad_grid(), 256, 0, stream>>>(p, ppad, pl);
+    SK_LAUNCH_CHECK("k_pad_fill");
+    return SK_OK;
   }
 
   // q = A p (+ p.q, alpha)
@@ -392,7 +534,11 @@ struct CgPlan {
     }
     const int f = launch_apply_pq(op.s, op.g, p, q, st, partials, stream);  // fused p.q (3D streaming stencils)
     if (f != kApplyPqUnsupported) return f;
-    if (int e = launch_apply(op.s, op.g, p, q, stream)) return e;
+    if (padded) {
+      if (int e = launch_apply_padded(op.s, op.g, ppad + pl.at(0, 0, 0), pl.px, pl.plane, q, stream)) return e;
+    } else if (int e = launch_apply(op.s, op.g, p, q, stream)) {
+      return e;
+    }
     k_pq<<<grid, kT, 0, stream>>>(n, p, q, st, partials);
     SK_LAUNCH_CHECK("k_pq");
     return SK_OK;
@@ -492,10 +638,16 @@ struct CgPlan {
     }
     if (int e = launch_q(cap)) return e;
     k2_update_rr<false, false><<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials, h);
-    if (cond)
+    if (padded) {
+      if (cond)
+        k3_xpby_pad<true><<<pad_grid(), 256, 0, cap>>>(r, p, ppad, pl, st, h);
+      else
+        k3_xpby_pad<false><<<pad_grid(), 256, 0, cap>>>(r, p, ppad, pl, st, h);
+    } else if (cond) {
       k3_xpby<true><<<grid, kT, 0, cap>>>(n, r, p, st, h);
-    else
+    } else {
       k3_xpby<false><<<grid, kT, 0, cap>>>(n, r, p, st, h);
+    }
     return SK_OK;
   }
   int build_loop_graph(double* x, cudaStream_t cap) {
@@ -560,6 +712,33 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
       pl->coop = pl->coop_grid > 0;
     }
   }
+  if (op.s && apply_padded_supported(op.s, op.g) && option(SK_OPT_CG_PADDED)) {
+    bool per = true;
+    for (int a = 0; a < 3; ++a) per &= op.g.bc[a] == SK_BC_PERIODIC;
+    PadLayout& L = pl->pl;
+    L.pad = 6;  // >= R + 1 (boundary + 4 ghosts), even: 16-byte aligned rows
+    L.R = 4;
+    for (int a = 0; a < 3; ++a) {
+      L.un[a] = op.g.un[a];
+      L.bc[a] = op.g.bc[a];
+    }
+    L.px = (op.g.un[0] + 2 * L.pad + 1) / 2 * 2;
+    L.py = op.g.un[1] + 2 * L.pad;
+    L.plane = L.px * L.py;
+    const size_t elems = size_t(L.plane) * size_t(op.g.un[2] + 2 * L.pad);
+    // the 8-byte boundary-map loader is the slow case; periodic grids already take the 16-byte path
+    if (!per && op.g.un[0] >= 4 && op.g.un[1] >= 4 && op.g.un[2] >= 4 && L.plane * (op.g.un[2] + 8) < (int64_t(1) << 31)) {
+      if (cudaMalloc(reinterpret_cast<void**>(&pl->ppad), elems * sizeof(double)) != cudaSuccess) {
+        delete pl;
+        return fail(SK_ERR_OUT_OF_MEMORY, "cg padded p");
+      }
+      if (cudaMemsetAsync(pl->ppad, 0, elems * sizeof(double), stream) != cudaSuccess) {
+        delete pl;
+        return fail(SK_ERR_CUDA, "cg padded p init");
+      }
+      pl->padded = true;
+    }
+  }
   if (op.m) {
     if (int e = csr_build_sell(const_cast<sk_csr*>(op.m), stream)) {  // before any graph capture
       delete pl;
@@ -612,6 +791,7 @@ int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options*
     if (int e = s->true_residual(x, b, &dummy, stream)) return e;
     k_restart<<<s->grid, kT, 0, stream>>>(n, b, s->q, s->r, s->p, s->st, s->partials);
     SK_LAUNCH_CHECK("k_restart");
+    if (int e = s->refresh_pad(stream)) return e;
     SK_CUDA_TRY(cudaMemcpyAsync(&rho0, &s->st->rho, sizeof(double), cudaMemcpyDeviceToHost, stream));
     SK_CUDA_TRY(cudaStreamSynchronize(stream));
   } else {
@@ -619,6 +799,7 @@ int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options*
     SK_CUDA_TRY(cudaMemsetAsync(x, 0, vec, stream));
     SK_CUDA_TRY(cudaMemcpyAsync(s->r, b, vec, cudaMemcpyDeviceToDevice, stream));
     SK_CUDA_TRY(cudaMemcpyAsync(s->p, b, vec, cudaMemcpyDeviceToDevice, stream));
+    if (int e = s->refresh_pad(stream)) return e;
   }
   const double target = opts.rel_tol * bnorm;
   CgState h{};
@@ -645,6 +826,7 @@ int cg_plan_solve(CgPlan* s, const double* b, double* x, const sk_solve_options*
       if (true_res <= target) break;
       k_restart<<<s->grid, kT, 0, stream>>>(n, b, s->q, s->r, s->p, s->st, s->partials);
       SK_LAUNCH_CHECK("k_restart");
+      if (int e = s->refresh_pad(stream)) return e;
       restarts++;
     }
     if (s->coop) {

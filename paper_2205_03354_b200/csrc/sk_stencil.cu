@@ -185,7 +185,7 @@ int launch_3d(Args3D a, cudaStream_t stream) {
   // rotated columns (seg_of: balanced ranges, neighbour tiles in phase);
   // z-ghosted slabs: lockstep for the radius-2 apply (halo rows from L2),
   // balanced otherwise
-  a.zrot = a.z_ghosted ? 0 : 1;
+  a.zrot = (a.z_ghosted && !a.in_pitch) ? 0 : 1;  // a padded field has its z halo: columns may rotate
   const int64_t grid = persistent_grid<C>(a, num_sms(), /*lockstep=*/!a.zrot && C::R == 2 && M == Mode::Apply);
   if (grid == 0) return fail(SK_ERR_INVALID_ARGUMENT, "grid too large for the 3D streaming kernels");
   if (a.bulk_ok)  // (after persistent_grid, which may clear it)
@@ -348,6 +348,39 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
     return launch_3d<Mode::Apply, C3R4>(a, stream);
   }
   return launch_generic(s, g, u, v, stream);
+}
+
+// Radius-4 apply from a ghost-padded field (matrix-free CG on non-periodic
+// grids, sk_cg.cu): u_origin points at interior (0,0,0) of a layout with row
+// pitch `pitch` and plane pitch `plane` whose halo (boundary zeros and the
+// reflected / wrapped images, PadLayout) is filled, so the 16-byte loader
+// runs without boundary maps. Same tile contents, hence the same bits, as
+// the boundary-mapped loader. kApplyPqUnsupported: not applicable.
+bool apply_padded_supported(const sk_stencil* s, const GridInfo& g) {
+  return s->kclass == 3 && g.dim == 3 && streamable(s, g, 4) && g.un[0] >= Cfg3R4P::TX + 2 * Cfg3R4P::R &&
+         g.un[1] >= Cfg3R4P::TY + 2 * Cfg3R4P::R;
+}
+
+int launch_apply_padded(const sk_stencil* s, const GridInfo& g, const double* u_origin, int64_t pitch,
+                        int64_t plane, double* v, cudaStream_t stream) {
+  if (!apply_padded_supported(s, g)) return kApplyPqUnsupported;
+  const double scale = pow_int(g.h, s->h_power);
+  Args3D a{};
+  a.u = u_origin;
+  a.v = v;
+  a.nx = g.un[0];
+  a.ny = g.un[1];
+  a.nz = g.un[2];
+  for (int i = 0; i < 3; ++i) a.bc[i] = g.bc[i];
+  for (int i = 0; i < 8; ++i) a.w[i] = s->orbit_coeff[i] * scale;
+  a.in_pitch = pitch;
+  a.in_plane = plane;
+  a.z_ghosted = 1;
+  a.bulk_ok = (pitch % 2 == 0) && (plane % 2 == 0) && aligned16(u_origin) && aligned16(v) &&
+              a.nx >= Cfg3R4P::TX + 2 * Cfg3R4P::R && a.ny >= Cfg3R4P::TY + 2 * Cfg3R4P::R &&
+              plane * (a.nz + 8) < (int64_t(1) << 31);
+  if (!a.bulk_ok) return kApplyPqUnsupported;
+  return launch_3d<Mode::Apply, Cfg3R4P>(a, stream);
 }
 
 // Matrix-free CG: q = A p fused with p.q -> alpha (stream3d_kernel<..., PQ>)

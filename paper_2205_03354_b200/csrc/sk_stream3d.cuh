@@ -80,6 +80,8 @@ struct Args3D {
   int ghost;         // chf3d OUT 1: ghost rows written on each side (2)
   int zrot;          // periodic z, zchunk = nz: every tile column is rotated so CTA range starts sit at
                      // the same planes in every column (seg_of): neighbour tiles are streamed in phase
+  int64_t in_pitch;  // != 0: u is a ghost-padded field (row pitch in_pitch, plane pitch in_plane, u at the
+  int64_t in_plane;  // interior origin, every halo point present): 16-byte loads without wrap (matrix-free CG)
 };
 
 // Host: tiles, persistent grid (min_blocks CTAs per SM, each a balanced
@@ -225,7 +227,7 @@ struct PlaneLoader {
     constexpr int R = C::R;
     x0 = x0_;
     y0 = y0_;
-    plane = a.u + int64_t(gz) * a.nx * a.ny;
+    plane = a.u + int64_t(gz) * (a.in_pitch ? a.in_plane : a.nx * a.ny);
     if constexpr (!FB) {
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
@@ -234,8 +236,12 @@ struct PlaneLoader {
         dst[k] = smem_u32(ring);
         if (used(k)) {
           const int r = i / HP, c = 2 * (i - r * HP);
-          const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
-          off[k] = int(gy * a.nx + gx);  // bulk path: nx * ny < 2^31
+          if (a.in_pitch) {  // ghost-padded input: the halo exists around the field
+            off[k] = int((y0 - R + r) * a.in_pitch + (x0 - R + c));
+          } else {
+            const int64_t gy = wrap1(y0 - R + r, a.ny), gx = wrap1(x0 - R + c, a.nx);
+            off[k] = int(gy * a.nx + gx);  // bulk path: nx * ny < 2^31
+          }
           dst[k] = smem_u32(ring + r * C::PITCH + c);
         }
       }
@@ -289,7 +295,7 @@ struct PlaneLoader {
         }
       }
     }
-    plane = (!a.z_ghosted && gz + 1 == a.nz) ? a.u : plane + a.nx * a.ny;
+    plane = (!a.z_ghosted && gz + 1 == a.nz) ? a.u : plane + (a.in_pitch ? a.in_plane : a.nx * a.ny);
   }
 };
 
@@ -529,7 +535,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS) stream3d_kernel(con
     bool row_ok[PY];
 #pragma unroll
     for (int j = 0; j < PY; ++j) row_ok[j] = gy0 + j < a.ny;
-    const bool vec_ok = a.bulk_ok && gx0 + PX <= a.nx;
+    const bool vec_ok = a.bulk_ok && !(a.nx & 1) && gx0 + PX <= a.nx;  // 16-byte stores need even rows (padded input may be odd)
     double* outp = a.v + int64_t(sg.z0) * plane_sz + gy0 * a.nx + gx0;  // output plane z0, first owned point
     const int np = int(sg.len) + 2 * R;
     for (int pb = 0; pb < np; pb += Q) {

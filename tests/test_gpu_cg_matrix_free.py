@@ -107,3 +107,27 @@ def test_3d_apply_pq_matches_separate_pass(sk_option, bc, check_every):
     assert abs(reps[0].iterations - reps[1].iterations) <= 2
     assert reps[0].true_rel_residual <= 1e-9
     assert np.linalg.norm(xs[0] - xs[1]) <= 1e-7 * np.linalg.norm(xs[1])
+
+
+@pytest.mark.parametrize("dims,bcs", [((75, 19, 19), ("clamped",) * 3), ((81, 20, 19), ("simply_supported",) * 3),
+                                      ((70, 33, 17), ("clamped", "periodic", "simply_supported")),
+                                      ((64, 40, 24), ("periodic", "clamped", "clamped"))])
+def test_padded_p_cg_is_bit_identical(sk_option, dims, bcs):
+    # radius-4 matrix-free CG off periodic grids: the p-update kernel writes a
+    # ghost-padded copy of p (reflected / wrapped images, boundary zeros) and
+    # the apply reads it with the 16-byte loader; the tiles hold the same
+    # values as the boundary-mapped loader's, so every iterate is identical
+    from paper_2205_03354_b200.grid import GridSpec
+
+    bc = [getattr(BoundaryKind, b) for b in bcs]
+    n = [d + (2 if b != BoundaryKind.periodic else 0) for d, b in zip(dims, bc)]
+    g = GridSpec(dim=3, n=n, h=1.0 / 32, origin=[0.0] * 3, bc=bc)
+    assert g.unknown_count() == dims[0] * dims[1] * dims[2]
+    b = np.sin(np.arange(g.unknown_count()) * 0.013) + 1.0
+    o = SolveOptions(rel_tol=1e-9, accept_recurrence=True)
+    out = {}
+    for flag in (1, 0):
+        sk_option("cg_padded", flag)
+        rep = SolveReport()
+        out[flag] = (cg_solve_stencil(DeviceStencil(bilaplacian(3, 4)), g, b, o, rep), rep.iterations)
+    assert np.array_equal(out[1][0], out[0][0]) and out[1][1] == out[0][1]
