@@ -60,6 +60,10 @@ class SlabCahnHilliard:
         n = (self.nzl + 2 * GHOST) * self.plane
         self.buf = [torch.zeros(n, dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.float64, device=dev)]
         self.cur = 0
+        # gloo cannot send device tensors: stage the halo planes through host
+        # memory (NCCL exchanges device buffers directly)
+        self.host_staged = bool(self.dist) and self.dist.get_backend() == "gloo" and self.buf[0].is_cuda
+        self._stage = [torch.zeros(GHOST * self.plane, dtype=torch.float64) for _ in range(2)]
         if step_fn is None:
             self.lib = ensure_device()
             lap = laplacian(3, 2)
@@ -94,6 +98,16 @@ class SlabCahnHilliard:
             return
         down, up = (self.rank - 1) % self.world, (self.rank + 1) % self.world
         d = self.dist
+        if self.host_staged:  # gloo with device buffers: halo planes through pinned host copies
+            send = [lo_in.to("cpu"), hi_in.to("cpu")]
+            recv = [self._stage[0], self._stage[1]]
+            ops = [d.P2POp(d.isend, send[0], down), d.P2POp(d.isend, send[1], up),
+                   d.P2POp(d.irecv, recv[1], up), d.P2POp(d.irecv, recv[0], down)]
+            for r in d.batch_isend_irecv(ops):
+                r.wait()
+            lo_gh.copy_(recv[0])
+            hi_gh.copy_(recv[1])
+            return
         ops = [d.P2POp(d.isend, lo_in.contiguous(), down), d.P2POp(d.isend, hi_in.contiguous(), up),
                d.P2POp(d.irecv, hi_gh, up), d.P2POp(d.irecv, lo_gh, down)]
         for r in d.batch_isend_irecv(ops):
