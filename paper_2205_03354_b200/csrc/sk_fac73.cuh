@@ -46,6 +46,14 @@ namespace sk {
 #define SK_F2_TY 16
 #define SK_F2_S 8
 #endif
+// SK_F2_BSTAGE (experiment, off): border pairs read their z-neighbours from
+// the u stages (5 live stages) instead of a register queue, 20 fewer
+// registers; with 64 x 24 tiles that allows 12 warps per SM (166 registers,
+// 7 stages) but measured 94.4 vs 93.6 us: more warps do not help, the kernel
+// is bound by its shared-memory traffic (~100 KB per tile-plane)
+#ifndef SK_F2_BSTAGE
+#define SK_F2_BSTAGE 0
+#endif
 using CfgF2 = Cfg3<4, 64, SK_F2_TY, 2, 2, SK_F2_S, 1>;
 
 struct L4W {
@@ -115,7 +123,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
     }
     s_load = s_load + 1 == S ? 0 : s_load + 1;
   };
-  for (int k = 0; k < S - 3; ++k) issue();  // lookahead S - 3 planes (live stages: k-2, k-1, k)
+  constexpr int LIVE = SK_F2_BSTAGE ? 5 : 3;  // stages read per step: k-4..k (border z from stages) or k-2..k
+  for (int k = 0; k < S - LIVE; ++k) issue();  // lookahead S - LIVE planes
 
   const int cofs = (2 * ty + R) * P + 2 * lane + R;    // own point (row 0, col 0) in a u stage
   const int wofs = (2 * ty + 2) * WP + 2 * lane + 2;   // ... in a w slot
@@ -144,7 +153,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
   if (!has_b) b_r = cofs;  // harmless in-range offset (loads unused)
 
   double2 U[5][2], W[5][2];  // own u / w of plane j in [j % 5]: row 0 pair, row 1 pair
+#if !SK_F2_BSTAGE
   double2 UB[5];             // the border pair's u of plane j
+#endif
   int s_k = 0;               // stage of u plane k
   uint32_t fph = 0;          // parity of the current use of stage s_k
   int w_slot = 0;            // w slot of plane k-2 (written this step); plane k-4: w_slot - 2 (mod 4)
@@ -170,13 +181,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
         const double* cn = ring + s_k * PLANE;
         U[J0][0] = ld2(cn + cofs);
         U[J0][1] = ld2(cn + cofs + P);
+#if !SK_F2_BSTAGE
         UB[J0] = ld2(cn + b_r);
+#endif
       }
       const int s_k2 = s_k >= 2 ? s_k - 2 : s_k - 2 + S;  // stage of plane k-2
       // all warps past step t-1: the stage of plane k-3 and the w slot written below are free
       if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
       sk_jitter(51);
-      issue();  // plane k + S - 3 into the stage of plane k-3
+      issue();  // plane k + S - LIVE into the stage of plane k - LIVE (last read at step t-1)
       double* wsl = wring + w_slot * WPLANE;
       if (k >= 4) {  // w(k-2)
         const double* rc = ring + s_k2 * PLANE;
@@ -193,8 +206,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
         *reinterpret_cast<double2*>(wsl + wofs + WP) = W[J2][1];
         if (has_b) {
           const double* c = rc + b_r;
+#if SK_F2_BSTAGE
+          auto stz = [&](int back) { return ring + (s_k >= back ? s_k - back : s_k - back + S) * PLANE + b_r; };
+          const double2 wb = l4_pair(lw, ld2(c), ld2(c - 2), ld2(c + 2), ld2(c - P), ld2(c + P), ld2(c - 2 * P),
+                                     ld2(c + 2 * P), ld2(stz(3)), ld2(stz(1)), ld2(stz(4)), ld2(stz(0)));
+#else
           const double2 wb = l4_pair(lw, UB[J2], ld2(c - 2), ld2(c + 2), ld2(c - P), ld2(c + P), ld2(c - 2 * P),
                                      ld2(c + 2 * P), UB[J3], UB[J1], UB[J4], UB[J0]);
+#endif
           *reinterpret_cast<double2*>(wsl + b_w) = wb;
         }
       }
