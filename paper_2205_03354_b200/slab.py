@@ -114,6 +114,87 @@ class SlabCahnHilliard:
             r.wait()
 
     # ---- stepping ----
+    def _slab_call(self, src, dst, z0: int, count: int, dt: float, stream) -> None:
+        """The fused step on output planes [z0, z0 + count) of this slab: the same
+        kernel on a sub-slab (its two ghost planes each side lie in src)."""
+        from ._lib import GridDesc
+
+        d = GridDesc()
+        d.dim, d.h = self._desc.dim, self._desc.h
+        for a in range(3):
+            d.n[a], d.bc[a] = self._desc.n[a], self._desc.bc[a]
+        d.n[2] = count
+        p = self.plane * 8
+        check(self.lib.sk_ch_explicit_slab(self.lap.handle, self.bilap.handle, C.byref(d), C.byref(self._p), dt,
+                                           C.c_void_p(src.data_ptr() + z0 * p),
+                                           C.c_void_p(dst.data_ptr() + (GHOST + z0) * p), stream))
+
+    def step_overlapped(self, dt: float, nsteps: int = 1) -> None:
+        """Halo exchange overlapped with the interior: per step the planes the
+        neighbours need next (EDGE at each end) are computed first on one stream,
+        their exchange runs while the interior planes are computed on a second
+        stream, and the received planes land in the ghost frame of the output
+        buffer (which the interior kernel never touches). Each output plane is
+        computed once from the same inputs, so the result is bit-identical to
+        `step`. Exercised with host-staged gloo exchange (two ranks on one GPU,
+        tests/test_gpu_slab.py); with NCCL the boundary planes go device to
+        device on the boundary stream (needs two GPUs, not measured here)."""
+        import torch
+
+        EDGE = 3  # a sub-slab needs >= 3 planes (grid descriptor); the neighbours need 2
+        if self.step_fn is not None or self.nzl < 2 * EDGE + 1:
+            return self.step(dt, nsteps)
+        self.exchange()  # ghosts of the current buffer
+        lib = self.lib
+        sb, si = C.c_void_p(), C.c_void_p()
+        check(lib.sk_stream_create(C.byref(sb)))
+        check(lib.sk_stream_create(C.byref(si)))
+        p, g, nzl = self.plane, GHOST, self.nzl
+        try:
+            if self.host_staged:
+                pin = [torch.empty(g * p, dtype=torch.float64).pin_memory() for _ in range(2)]
+            for _ in range(nsteps):
+                src, dst = self.buf[self.cur], self.buf[1 - self.cur]
+                check(lib.sk_stream_sync(None))  # src complete (previous step, ghost copies)
+                self._slab_call(src, dst, 0, EDGE, dt, sb)
+                self._slab_call(src, dst, nzl - EDGE, EDGE, dt, sb)
+                self._slab_call(src, dst, EDGE, nzl - 2 * EDGE, dt, si)  # interior, concurrently
+                lo_in, hi_in = dst[g * p:2 * g * p], dst[nzl * p:(nzl + g) * p]
+                lo_gh, hi_gh = dst[0:g * p], dst[(nzl + g) * p:(nzl + 2 * g) * p]
+                if self.world == 1 or not self.host_staged:
+                    check(lib.sk_stream_sync(sb))
+                    if self.world == 1:
+                        lo_gh.copy_(hi_in)
+                        hi_gh.copy_(lo_in)
+                    else:  # NCCL: device buffers directly
+                        down, up = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+                        d = self.dist
+                        ops = [d.P2POp(d.isend, lo_in.contiguous(), down), d.P2POp(d.isend, hi_in.contiguous(), up),
+                               d.P2POp(d.irecv, hi_gh, up), d.P2POp(d.irecv, lo_gh, down)]
+                        for r in d.batch_isend_irecv(ops):
+                            r.wait()
+                else:
+                    for k, src_dev in enumerate((lo_in, hi_in)):  # boundary planes to pinned host, stream sb
+                        check(lib.sk_memcpy_d2h(C.c_void_p(pin[k].data_ptr()), C.c_void_p(src_dev.data_ptr()),
+                                                g * p * 8, sb))
+                    check(lib.sk_stream_sync(sb))  # (the interior kernel keeps running on si)
+                    down, up = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+                    d = self.dist
+                    recv = [self._stage[0], self._stage[1]]
+                    ops = [d.P2POp(d.isend, pin[0], down), d.P2POp(d.isend, pin[1], up),
+                           d.P2POp(d.irecv, recv[1], up), d.P2POp(d.irecv, recv[0], down)]
+                    for r in d.batch_isend_irecv(ops):
+                        r.wait()
+                    for k, dst_dev in enumerate((lo_gh, hi_gh)):
+                        check(lib.sk_memcpy_h2d(C.c_void_p(dst_dev.data_ptr()), C.c_void_p(recv[k].data_ptr()),
+                                                g * p * 8, sb))
+                check(lib.sk_stream_sync(sb))
+                check(lib.sk_stream_sync(si))
+                self.cur = 1 - self.cur
+        finally:
+            lib.sk_stream_destroy(sb)
+            lib.sk_stream_destroy(si)
+
     def step(self, dt: float, nsteps: int = 1) -> None:
         for _ in range(nsteps):
             self.exchange()

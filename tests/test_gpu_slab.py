@@ -29,7 +29,7 @@ def test_slab_single_rank_equals_single_domain(dims, formulation):
     assert np.array_equal(s.local_field(), st.c)
 
 
-def _cuda_slab_worker(rank, world, port, dims, steps, out):
+def _cuda_slab_worker(rank, world, port, dims, steps, out, overlapped=False):
     import os
     import sys
 
@@ -48,13 +48,18 @@ def _cuda_slab_worker(rank, world, port, dims, steps, out):
     g = GridSpec(dim=3, n=list(dims), h=h, origin=[0.0] * 3, bc=[BoundaryKind.periodic] * 3)
     s = SlabCahnHilliard(g, p)  # the CUDA slab step (sk_ch_explicit_slab) on cuda:0
     s.scatter(0.05 * np.random.default_rng(11).uniform(-1, 1, g.unknown_count()))
-    s.step(0.2 * h ** 4 / (144 * p.kappa), steps)
+    dt = 0.2 * h ** 4 / (144 * p.kappa)
+    if overlapped:
+        s.step_overlapped(dt, steps)
+    else:
+        s.step(dt, steps)
     out[rank] = s.local_field()
     dist.destroy_process_group()
 
 
 @pytest.mark.timeout(300)
-def test_slab_two_cuda_ranks_equal_single_domain():
+@pytest.mark.parametrize("overlapped", [False, True])
+def test_slab_two_cuda_ranks_equal_single_domain(overlapped):
     # two ranks (processes) each run the CUDA slab step on its half of the z
     # planes — both on the one GPU here, independent kernels, the halo planes
     # exchanged over gloo through host memory — and reproduce the
@@ -73,7 +78,7 @@ def test_slab_two_cuda_ranks_equal_single_domain():
     dims, steps, world = (64, 64, 32), 12, 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_cuda_slab_worker, args=(world, free_port(), dims, steps, out), nprocs=world, join=True)
+    mp.spawn(_cuda_slab_worker, args=(world, free_port(), dims, steps, out, overlapped), nprocs=world, join=True)
     got = np.concatenate([out[r] for r in range(world)])
     p = CahnHilliardParams.from_epsilon(0.02)
     h = 1.0 / max(dims)
@@ -81,3 +86,19 @@ def test_slab_two_cuda_ranks_equal_single_domain():
     st = CahnHilliardState(g, 0.05 * np.random.default_rng(11).uniform(-1, 1, g.unknown_count()))
     CahnHilliardExplicit(g, p).step(st, 0.2 * h ** 4 / (144 * p.kappa), steps)
     assert np.array_equal(got, st.c)
+
+
+def test_slab_overlapped_single_rank_equals_single_domain():
+    # the boundary / interior split on one rank (periodic self-exchange)
+    dims = (64, 64, 32)
+    p = CahnHilliardParams.from_epsilon(0.02)
+    h = 1.0 / max(dims)
+    dt = 0.2 * h ** 4 / (144 * p.kappa)
+    g = GridSpec(dim=3, n=list(dims), h=h, origin=[0.0] * 3, bc=[BoundaryKind.periodic] * 3)
+    c0 = 0.05 * np.random.default_rng(12).uniform(-1, 1, g.unknown_count())
+    s = SlabCahnHilliard(g, p)
+    s.scatter(c0)
+    s.step_overlapped(dt, 15)
+    st = CahnHilliardState(g, c0.copy())
+    CahnHilliardExplicit(g, p).step(st, dt, 15)
+    assert np.array_equal(s.local_field(), st.c)
