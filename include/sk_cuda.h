@@ -311,7 +311,8 @@ int sk_cg_solve_stencil(const sk_stencil* s, const sk_grid_desc* g, const double
  * sk_residual_refined: r = b - A x with the
  * exact weights, evaluated in double-double (error-free products and
  * compensated sums), rounded to fp64. sk_cg_solve_stencil_refined: the
- * matrix-free CG (opts) followed by up to max_refinements steps
+ * matrix-free CG (opts, stopping on the recurrence residual) followed by up
+ * to max_refinements steps
  * x += CG(A_fl, r_refined) with inner tolerance inner_rel_tol (recurrence
  * criterion), stopping when ||d|| <= 1e-15 ||x||. */
 typedef struct sk_refine_report {
