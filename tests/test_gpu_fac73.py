@@ -55,7 +55,7 @@ def test_fac73_smooth_input(orc, sk_option):
 
 def test_fac73_not_used_off_periodic(orc, sk_option):
     # clamped grids keep the literal kernel (the factorisation does not hold at
-    # reflected boundaries): SK_F73 has no effect there
+    # reflected boundaries): SK_OPT_APPLY73_FACTORED has no effect there
     g = GridSpec(dim=3, n=[41, 41, 41], h=1.0 / 40, origin=[0.0] * 3, bc=[BoundaryKind.clamped] * 3)
     s = bilaplacian(3, 4)
     u = np.random.default_rng(3).uniform(-1, 1, g.unknown_count())

@@ -1,8 +1,9 @@
 #!/usr/bin/env python3
-"""Small invocations of every device path, for compute-sanitizer
-(memcheck / racecheck / synccheck / initcheck) runs:
+"""Small invocations of every device path, each checked against the oracle —
+for tools that wrap a whole program (compute-sanitizer where it is available;
+it is closed on this GPU pool, see profiles/r2_race_and_guards.md):
 
-    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitizer_cases.py
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/device_cases.py
 
 Covers: the ghost-padded TMA chunk of the 3D CH step (mbarrier ring, PDL
 chain), the plain cp.async CH kernels (2D and 3D, composed and factored), the
@@ -11,8 +12,8 @@ every boundary kind, the last-CTA reductions (dot / nrm2 / sum / minmax / free
 energy), CSR assembly + SELL SpMV, the device CG loop (CSR, matrix-free 2D
 fused + cooperative, 3D with p.q in the apply epilogue), an IMEX step, and
 power iteration. Each case also checks its result against the oracle, so a
-sanitizer run is also a parity run. Sizes are tiny: the tools slow kernels
-down by 10-100x.
+wrapped run is also a parity run. Sizes are tiny (sanitizers slow kernels
+down by 10-100x).
 """
 from __future__ import annotations
 
@@ -139,7 +140,7 @@ def main() -> int:
     assert abs(lam - 64.0) <= 1e-6 * 64.0  # 13-point symbol max (4 + 4)^2 at h = 1
     done.append("imex+power")
 
-    print("sanitizer cases ok:", ", ".join(done), f"({lib.sk_launch_count()} kernel launches)")
+    print("device cases ok:", ", ".join(done), f"({lib.sk_launch_count()} kernel launches)")
     return 0
 
 
