@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           if (lane == 0) {  // the producer: lane 0 of warp t % WARPS (the others advance their cursor copies)
             if (ty == prod) {
               sk_jitter(13);
-              fence_proxy_async_smem();
+              tma_war_fence();
               tc.issue_next(ring, bars, s_iss, a, &tmap);
             } else {
               tc.template issue_next<false>(ring, bars, s_iss, a, &tmap);
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
 #else
           if (threadIdx.x == 0) {  // stage of plane k-3 is free (last read at step t-1)
             sk_jitter(13);
-            fence_proxy_async_smem();
+            tma_war_fence();
             tc.issue_next(ring, bars, s_iss, a, &tmap);
           }
 #endif

@@ -157,6 +157,21 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst_smem, const void* tma
 // order this thread's prior generic-proxy shared accesses before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Before a TMA refill of a ring slot that generic loads read earlier (WAR).
+// The reads are ordered before the refill by the mbarrier that frees the slot
+// (every reader arrives, release; the producer waits, acquire) -- the usual
+// TMA-pipeline hand-off. An explicit proxy fence (-DSK_TMA_WAR_FENCE=1)
+// compiles to MEMBAR.ALL.CTA, which also waits for the producer thread's
+// outstanding global stores: measured 55.3 vs 54.9 us per 256^3 CH step.
+#ifndef SK_TMA_WAR_FENCE
+#define SK_TMA_WAR_FENCE 0
+#endif
+__device__ __forceinline__ void tma_war_fence() {
+#if SK_TMA_WAR_FENCE
+  fence_proxy_async_smem();
+#endif
+}
+
 // Per-thread asynchronous global->shared copies (LDGSTS), L1-bypassing.
 __device__ __forceinline__ void cp_async16(void* dst_smem, const void* src_gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
