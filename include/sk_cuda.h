@@ -166,7 +166,8 @@ enum sk_option {
   SK_OPT_IMEX_MATRIX_FREE = 6, /* IMEX implicit operator applied matrix-free (0: CSR SpMV): 1 */
   SK_OPT_APPLY73_FACTORED = 7, /* periodic 73-point apply as L4(L4 u) (0: literal 73 weights): 1 */
   SK_OPT_CG_PADDED = 8,        /* radius-4 matrix-free CG off periodic grids: ghost-padded p (16-byte loads): 1 */
-  SK_OPT_COUNT = 9
+  SK_OPT_CH_HOST_PIPELINE = 9, /* sk_ch_explicit_host (3D, pinned host field): upload / steps / download overlapped: 1 */
+  SK_OPT_COUNT = 10
 };
 int sk_set_option(int option, int value);
 int sk_get_option(int option, int* value);
@@ -204,6 +205,11 @@ int sk_composed_apply_host(const sk_stencil* s, const sk_grid_desc* g, const dou
 int sk_ch_explicit(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
                    const sk_ch_params* p, double dt, int64_t nsteps, double* c_dev,
                    double* scratch_dev, int* result_is_scratch, void* stream);
+/* The same from host memory: c_host in, K steps, result back in c_host.
+ * With a pinned (or sk_host_register'ed) 3D field of nz >= 4K + 8 planes the
+ * upload, the steps and the download overlap (plane chunks; each step's
+ * front advances as the planes it depends on arrive); the result is
+ * bit-identical to the serial H2D -> steps -> D2H. */
 int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
                         const sk_ch_params* p, double dt, int64_t nsteps, double* c_host);
 /* One fused explicit step on a z-slab of a periodic 3D field (multi-GPU slab

@@ -145,7 +145,8 @@ def load(path: Optional[Path] = None) -> C.CDLL:
 
 # sk_set_option ids (include/sk_cuda.h enum sk_option)
 OPTIONS = {"pdl": 0, "ch_padded": 1, "cg_device_loop": 2, "cg_fused": 3, "cg_coop": 4, "cg_pq": 5,
-           "imex_matrix_free": 6, "apply73_factored": 7, "cg_padded": 8}
+           "imex_matrix_free": 6, "apply73_factored": 7, "cg_padded": 8,
+           "ch_host_pipeline": 9}
 
 
 def set_option(name: str, value: int) -> int:

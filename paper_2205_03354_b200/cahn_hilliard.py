@@ -81,6 +81,15 @@ class CahnHilliardExplicit:
                                       dt, nsteps, c.ptr, scratch.ptr, C.byref(which), stream))
         return scratch if which.value else c
 
+    def run_host(self, c: np.ndarray, dt: float, nsteps: int) -> None:
+        """nsteps steps on a contiguous float64 host field, in place. A pinned or
+        registered field (kernels.host_register) of a 3D grid with nz >= 4 nsteps + 8
+        overlaps the upload, the steps and the download (sk_ch_explicit_host)."""
+        if c.dtype != np.float64 or not c.flags.c_contiguous or c.size != self.grid.unknown_count():
+            raise StencilkitError(Errc.shape_mismatch, "host field must be contiguous float64 of the grid's size")
+        check(self.lib.sk_ch_explicit_host(self.lap.handle, self.bilap.handle, C.byref(self._desc),
+                                           C.byref(self._p), dt, nsteps, c.ctypes.data))
+
     def step(self, state: CahnHilliardState, dt: float, nsteps: int = 1) -> None:
         """Host state in/out (the reference-facing call): copies in, steps, copies out."""
         if not dt > 0:

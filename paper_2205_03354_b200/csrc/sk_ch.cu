@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -350,6 +351,179 @@ ChCache& ch_cache() {
   return *c;
 }
 
+// ---- host entry point: copies overlapped with the steps (z wavefront) -----
+// A K-step call from host memory is PCIe-bound (a 256^3 field is 134 MB each
+// way at ~54 GB/s against ~1.1 ms for 20 steps). Output plane z of step s
+// depends only on input planes z-2s .. z+2s, so the field is uploaded in
+// plane chunks on one stream while a second stream advances every step's
+// front as far as the planes present allow and a third stream downloads the
+// final step's planes as they complete: upload, stepping and download
+// overlap.
+//
+// The periodic z axis is unrolled into a line of nz + T planes, T = 4K:
+// positions [nz, nz + T) hold copies of planes [0, T) (device copies made as
+// those planes land). On the line no step needs a wrap: step s produces
+// positions [2s, P - 2s) once positions [0, P) are present, as slab launches
+// on z ranges (in-buffer halos); the final step's positions [2K, nz + 2K) are
+// the field, the last 2K of them planes 0 .. 2K-1. When the upload ends only
+// the fronts' last C + T positions per step remain -- no ghost exchange, no
+// per-step seam work. (The 2K^2 redundant plane-steps cost ~16% more
+// stepping at K = 20, off the PCIe-bound critical path.)
+//
+// Ping-pong safety: step s writes buffer s % 2, which holds step s-2. Its
+// front trails step s-1's by 2 positions at both ends, so every position it
+// overwrites has already been consumed by step s-1; the tail copies of a
+// chunk are made before the chunk's fronts run. Every plane is computed by
+// the same kernel arithmetic as the serial path, so the result is
+// bit-identical (tests/test_gpu_ch_host.py).
+struct HostPipe {
+  cudaStream_t up = nullptr, run = nullptr, down = nullptr;
+  std::vector<cudaEvent_t> ev;
+  double* buf = nullptr;
+  size_t elems = 0;  // per buffer
+  int init() {
+    if (up) return SK_OK;
+    SK_CUDA_TRY(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    SK_CUDA_TRY(cudaStreamCreateWithFlags(&run, cudaStreamNonBlocking));
+    SK_CUDA_TRY(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    return SK_OK;
+  }
+  int event(size_t i, cudaEvent_t* out) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      SK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    *out = ev[i];
+    return SK_OK;
+  }
+  int reserve(size_t n) {
+    if (elems >= n) return SK_OK;
+    if (buf) SK_CUDA_TRY(cudaFree(buf));
+    buf = nullptr;
+    elems = 0;
+    SK_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&buf), 2 * n * sizeof(double)));
+    elems = n;
+    return SK_OK;
+  }
+};
+
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// eligible: 3D fast path, enough planes for the fronts to move (nz >= 4K + 8)
+static bool ch_host_pipelined_ok(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, int64_t nsteps,
+                                 const double* c_host) {
+  return option(SK_OPT_CH_HOST_PIPELINE) && g.dim == 3 && nsteps >= 1 && is_lap_shape(lap, 3) &&
+         is_bilap_shape(bilap, 3) && g.n[2] >= 4 * nsteps + 8 && host_pinned(c_host);
+}
+
+static int ch_host_pipelined(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
+                             double dt, int64_t nsteps, double* c_host) {
+  thread_local HostPipe hp;
+  if (int st = hp.init()) return st;
+  const int64_t nz = g.n[2], plane = g.n[0] * g.n[1], S = nsteps;
+  const int64_t T = 4 * S, L = nz + T;  // the unrolled line (T <= nz - 8: ch_host_pipelined_ok)
+  if (int st = hp.reserve(size_t(L * plane))) return st;
+  double* X[2] = {hp.buf, hp.buf + hp.elems};
+  const size_t pb = size_t(plane) * sizeof(double);
+  // one range [z0, z1) of step s (1-based) on the line: X[(s-1)%2] -> X[s%2], halos in the buffer
+  auto range = [&](int64_t s, int64_t z0, int64_t z1) -> int {
+    if (z1 <= z0) return SK_OK;
+    GridInfo gr = g;
+    gr.n[2] = gr.un[2] = z1 - z0;
+    gr.rows = plane * (z1 - z0);
+    return ch_step_fast(lap, bilap, gr, p, dt, X[(s - 1) % 2] + z0 * plane, X[s % 2] + z0 * plane, hp.run, true,
+                        kIoPlain, /*z_ghosted=*/true);
+  };
+  size_t nev = 0;
+  auto handoff = [&](cudaStream_t from, cudaStream_t to) -> int {  // `to` waits for `from`'s work so far
+    cudaEvent_t e;
+    if (int st = hp.event(nev++, &e)) return st;
+    SK_CUDA_TRY(cudaEventRecord(e, from));
+    SK_CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
+    return SK_OK;
+  };
+  auto download = [&](int64_t a, int64_t b) -> int {  // final-step positions [a, b) -> planes (mod nz)
+    for (int64_t lo = a; lo < b;) {
+      const int64_t hi = lo < nz ? std::min(b, nz) : b, z = lo < nz ? lo : lo - nz;
+      SK_CUDA_TRY(cudaMemcpyAsync(c_host + z * plane, X[S % 2] + lo * plane, size_t(hi - lo) * pb,
+                                  cudaMemcpyDeviceToHost, hp.down));
+      lo = hi;
+    }
+    return SK_OK;
+  };
+#ifdef SK_PIPE_TRACE  // tools-only timeline (tools/ab_build.py ... -DSK_PIPE_TRACE)
+  std::vector<std::pair<std::string, cudaEvent_t>> tr;
+  auto mark = [&](const std::string& what, cudaStream_t s) {
+    cudaEvent_t e = nullptr;
+    const cudaError_t c1 = cudaEventCreate(&e);
+    const cudaError_t c2 = cudaEventRecord(e, s);
+    if (c1 != cudaSuccess || c2 != cudaSuccess)
+      fprintf(stderr, "[pipe] mark %s: %s / %s\n", what.c_str(), cudaGetErrorString(c1), cudaGetErrorString(c2));
+    tr.push_back({what, e});
+  };
+#else
+  auto mark = [](const auto&, cudaStream_t) {};
+#endif
+  // the calling thread's earlier work on the shared streams is ordered before this call
+  if (int st = handoff(host_stream(), hp.up)) return st;
+  mark("start", hp.up);
+  // ~8 upload chunks (>= 8 planes each: fewer, larger launches for the fronts).
+  // Measured at 256^3 x 20 (B200, PCIe Gen5): 4.5-4.8 ms against 6.15 ms for
+  // the serial call. The stepping keeps pace with the upload until the last
+  // chunk; then its cone (C + 4K positions per step, 0.7 ms) and the download
+  // of the final C + 4K planes (1.1 ms) remain. Splitting the last chunk
+  // finer (C/2, C/4, ...) measured slower: each round is K launches.
+  const int64_t C = std::max<int64_t>(8, (nz + 7) / 8);
+  std::vector<int64_t> hi(size_t(S) + 1);
+  for (int64_t s = 1; s <= S; ++s) hi[size_t(s)] = 2 * s;
+  int64_t done = 2 * S;  // final-step positions downloaded: [2S, done)
+  for (int64_t z0 = 0; z0 < nz; z0 += C) {
+    const int64_t z1 = std::min(nz, z0 + C);
+    SK_CUDA_TRY(cudaMemcpyAsync(X[0] + z0 * plane, c_host + z0 * plane, size_t(z1 - z0) * pb,
+                                cudaMemcpyHostToDevice, hp.up));
+    mark("up " + std::to_string(z1), hp.up);
+    if (int st = handoff(hp.up, hp.run)) return st;
+    if (z0 < T)  // this chunk's share of the tail copies, before any front overwrites buffer 0
+      SK_CUDA_TRY(cudaMemcpyAsync(X[0] + (nz + z0) * plane, X[0] + z0 * plane, size_t(std::min(z1, T) - z0) * pb,
+                                  cudaMemcpyDeviceToDevice, hp.run));
+    const int64_t P = z1 == nz ? L : z1;  // positions present
+    for (int64_t s = 1; s <= S; ++s) {    // each front as far as the positions present allow
+      const int64_t top = P - 2 * s;
+      if (top > hi[size_t(s)]) {
+        if (int st = range(s, hi[size_t(s)], top)) return st;
+        hi[size_t(s)] = top;
+      }
+    }
+    if (hi[size_t(S)] - done >= C / 2 || z1 == nz) {
+      if (int st = handoff(hp.run, hp.down)) return st;
+      if (int st = download(done, hi[size_t(S)])) return st;
+      mark("down " + std::to_string(hi[size_t(S)]), hp.down);
+      done = hi[size_t(S)];
+    }
+    mark("fronts " + std::to_string(z1), hp.run);
+  }
+  mark("down end", hp.down);
+  SK_CUDA_TRY(cudaStreamSynchronize(hp.down));
+  SK_CUDA_TRY(cudaStreamSynchronize(hp.run));
+#ifdef SK_PIPE_TRACE
+  for (auto& m : tr) {
+    float ms = 0;
+    const cudaError_t e = cudaEventElapsedTime(&ms, tr[0].second, m.second);
+    fprintf(stderr, "[pipe] %-14s %8.3f ms %s\n", m.first.c_str(), ms, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  }
+  for (auto& m : tr) cudaEventDestroy(m.second);
+#endif
+  return SK_OK;
+}
+
 }  // namespace sk
 
 using namespace sk;
@@ -513,6 +687,14 @@ int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk
   if (!c_host && g.rows > 0) return fail(SK_ERR_INVALID_ARGUMENT, "null host field");
   if (nsteps < 0) return fail(SK_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
   if (g.rows == 0) return SK_OK;
+  if (nsteps > 0 && lap && bilap && p && dt > 0 && g.dim == 3) {
+    bool periodic = true;
+    for (int a = 0; a < 3; ++a) periodic = periodic && g.bc[a] == SK_BC_PERIODIC;
+    if (periodic && check_width(lap, g) == SK_OK && check_width(bilap, g) == SK_OK &&
+        (p->formulation == SK_CH_FACTORED || p->formulation == SK_CH_COMPOSED) &&
+        ch_host_pipelined_ok(lap, bilap, g, nsteps, c_host))
+      return ch_host_pipelined(lap, bilap, g, p, dt, nsteps, c_host);
+  }
   // c_host -> c (device), steps ping-pong c <-> s, result -> c_host. The
   // device pair is per host thread and kept between calls, so repeated calls
   // replay the cached chunk graphs (keyed by the buffers) instead of

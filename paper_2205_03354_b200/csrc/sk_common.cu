@@ -19,7 +19,7 @@ std::atomic<int64_t> g_launches{0};
 namespace {
 // sk_set_option values (include/sk_cuda.h enum sk_option order); defaults
 // are the measured-fastest paths
-std::atomic<int> g_options[SK_OPT_COUNT] = {1, 1, 1, 1, -1, 1, 1, 1, 1};
+std::atomic<int> g_options[SK_OPT_COUNT] = {1, 1, 1, 1, -1, 1, 1, 1, 1, 1};
 std::atomic<uint64_t> g_option_epoch{0};
 }  // namespace
 

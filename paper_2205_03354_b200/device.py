@@ -56,3 +56,21 @@ class DeviceArray:
 
     def __len__(self) -> int:
         return self.count
+
+
+class pinned:
+    """Page-lock a contiguous numpy array for the duration of a `with` block
+    (sk_host_register / sk_host_unregister), so host entry points can overlap
+    their copies with device work."""
+
+    def __init__(self, arr: np.ndarray):
+        if not arr.flags.c_contiguous:
+            raise ValueError("pinned() needs a contiguous array")
+        self.arr = arr
+
+    def __enter__(self) -> np.ndarray:
+        check(ensure_device().sk_host_register(self.arr.ctypes.data, self.arr.nbytes))
+        return self.arr
+
+    def __exit__(self, *exc) -> None:
+        check(ensure_device().sk_host_unregister(self.arr.ctypes.data))
