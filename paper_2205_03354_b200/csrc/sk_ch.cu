@@ -476,11 +476,12 @@ static int ch_host_pipelined(const sk_stencil* lap, const sk_stencil* bilap, con
   if (int st = handoff(host_stream(), hp.up)) return st;
   mark("start", hp.up);
   // ~8 upload chunks (>= 8 planes each: fewer, larger launches for the fronts).
-  // Measured at 256^3 x 20 (B200, PCIe Gen5): 4.5-4.8 ms against 6.15 ms for
+  // Measured at 256^3 x 20 (B200, PCIe Gen5): 4.3-4.4 ms against 6.15 ms for
   // the serial call. The stepping keeps pace with the upload until the last
-  // chunk; then its cone (C + 4K positions per step, 0.7 ms) and the download
-  // of the final C + 4K planes (1.1 ms) remain. Splitting the last chunk
-  // finer (C/2, C/4, ...) measured slower: each round is K launches.
+  // chunk; then its cone (C + 4K positions per step) is stepped in two passes
+  // so the lower half's final planes go down while the upper half is stepped
+  // (4.5-4.8 ms in one pass). Splitting the last chunk finer (C/2, C/4, ...)
+  // measured slower: each round is K launches.
   const int64_t C = std::max<int64_t>(8, (nz + 7) / 8);
   std::vector<int64_t> hi(size_t(S) + 1);
   for (int64_t s = 1; s <= S; ++s) hi[size_t(s)] = 2 * s;
@@ -495,13 +496,24 @@ static int ch_host_pipelined(const sk_stencil* lap, const sk_stencil* bilap, con
       SK_CUDA_TRY(cudaMemcpyAsync(X[0] + (nz + z0) * plane, X[0] + z0 * plane, size_t(std::min(z1, T) - z0) * pb,
                                   cudaMemcpyDeviceToDevice, hp.run));
     const int64_t P = z1 == nz ? L : z1;  // positions present
-    for (int64_t s = 1; s <= S; ++s) {    // each front as far as the positions present allow
-      const int64_t top = P - 2 * s;
-      if (top > hi[size_t(s)]) {
-        if (int st = range(s, hi[size_t(s)], top)) return st;
-        hi[size_t(s)] = top;
+    auto fronts = [&](int64_t cap) -> int {  // every front up to P - 2s, and for the final step below cap
+      for (int64_t s = 1; s <= S; ++s) {
+        const int64_t top = std::min(P - 2 * s, cap + 2 * (S - s));
+        if (top > hi[size_t(s)]) {
+          if (int st = range(s, hi[size_t(s)], top)) return st;
+          hi[size_t(s)] = top;
+        }
       }
+      return SK_OK;
+    };
+    if (z1 == nz) {  // the last cone in two passes: the lower half's planes go down during the upper pass
+      const int64_t mid = (hi[size_t(S)] + (P - 2 * S)) / 2;
+      if (int st = fronts(mid)) return st;
+      if (int st = handoff(hp.run, hp.down)) return st;
+      if (int st = download(done, hi[size_t(S)])) return st;
+      done = hi[size_t(S)];
     }
+    if (int st = fronts(L)) return st;
     if (hi[size_t(S)] - done >= C / 2 || z1 == nz) {
       if (int st = handoff(hp.run, hp.down)) return st;
       if (int st = download(done, hi[size_t(S)])) return st;
