@@ -57,9 +57,6 @@ constexpr int kPadL = SK_PADL, kPadT = 2;  // ghost rows above and below (the ra
 #ifndef SK_MU_SLOTS
 #define SK_MU_SLOTS 3
 #endif
-#ifndef SK_TMA_ROTATE
-#define SK_TMA_ROTATE 0  // experiment: the TMA producer rotates over the warps (measured: see DESIGN)
-#endif
 #ifndef SK_TMA_SPLIT
 #define SK_TMA_SPLIT 1
 #endif
@@ -110,19 +107,15 @@ struct TmaCursor {
     lp = 0;
     np = sg.len + 2 * C::R;
   }
-  // ISSUE false: only advance (the cursor copies of the non-producing warps, SK_TMA_ROTATE)
-  template <bool ISSUE = true>
   __device__ __forceinline__ void issue_next(double* ring, uint64_t* bars, int stage, const Args3D& a,
                                              const CUtensorMap* tm) {
     using SM = ChfSmem<C, 1>;
     if (u < uend) {
-      if constexpr (ISSUE) {
-        mbar_arrive_expect_tx(&bars[stage], SM::STAGE_BYTES);
+      mbar_arrive_expect_tx(&bars[stage], SM::STAGE_BYTES);
 #pragma unroll
-        for (int q = 0; q < kTmaSplit; ++q)  // the box: C::ROWS / kTmaSplit rows
-          tma_load_3d_hint<SK_TMA_HINT>(ring + stage * SM::PLANE + q * (C::ROWS / kTmaSplit) * SM::P, tm, x0,
-                                        y0 + q * (C::ROWS / kTmaSplit), z, &bars[stage]);
-      }
+      for (int q = 0; q < kTmaSplit; ++q)  // the box: C::ROWS / kTmaSplit rows
+        tma_load_3d_hint<SK_TMA_HINT>(ring + stage * SM::PLANE + q * (C::ROWS / kTmaSplit) * SM::P, tm, x0,
+                                      y0 + q * (C::ROWS / kTmaSplit), z, &bars[stage]);
       z = z + 1 == a.nz ? 0 : z + 1;
       if (++lp == np) {
         u += np - 2 * C::R;
@@ -189,20 +182,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
       s_load = s_load + 1 == S ? 0 : s_load + 1;
     }
   } else {
-#if SK_TMA_ROTATE
-    if (threadIdx.x % 32 == 0) {  // every warp's lane 0 tracks the cursor; the producer rotates per step
-#else
-    if (threadIdx.x == 0) {
-#endif
+    if (threadIdx.x == 0) {  // the producer
       tc.u = ubeg;
       tc.uend = uend;
       if (ubeg < uend) tc.start(a);
-      for (int k = 0; k < S - 3; ++k) {
-        if (threadIdx.x == 0)
-          tc.issue_next(ring, bars, k, a, &tmap);
-        else
-          tc.template issue_next<false>(ring, bars, k, a, &tmap);
-      }
+      for (int k = 0; k < S - 3; ++k) tc.issue_next(ring, bars, k, a, &tmap);
     }
     s_load = S - 3;
   }
@@ -250,9 +234,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   int sb = 0;                // t % 3
   uint32_t sph = 0;          // (t / 3) & 1
   bool started = false;      // t > 0
-#if SK_TMA_ROTATE
-  int prod = 0;              // producing warp of this step
-#endif
   for (int u = ubeg; u < uend; ) {
     const Seg sg = seg_of<C>(a, u, uend);
     u += sg.len;
@@ -359,24 +340,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
           if (started) mbar_wait(&stepbar[sb == 0 ? 2 : sb - 1], sb == 0 ? sph ^ 1u : sph);
         }
         if constexpr (LD == 1) {
-#if SK_TMA_ROTATE
-          if (lane == 0) {  // the producer: lane 0 of warp t % WARPS (the others advance their cursor copies)
-            if (ty == prod) {
-              sk_jitter(13);
-              tma_war_fence();
-              tc.issue_next(ring, bars, s_iss, a, &tmap);
-            } else {
-              tc.template issue_next<false>(ring, bars, s_iss, a, &tmap);
-            }
-          }
-          prod = prod + 1 == SM::WARPS ? 0 : prod + 1;
-#else
           if (threadIdx.x == 0) {  // stage of plane k-3 is free (last read at step t-1)
             sk_jitter(13);
             tma_war_fence();
             tc.issue_next(ring, bars, s_iss, a, &tmap);
           }
-#endif
         }
         if constexpr (DO_OUT && V == 0) out_neighbours();
         started = true;

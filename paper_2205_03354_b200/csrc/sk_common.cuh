@@ -102,17 +102,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef SK_MBAR_SUSPEND  // experiment: suspend-time hint (ns) instead of a bare spin
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(SK_MBAR_SUSPEND)
-      : "memory");
-#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -122,7 +111,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
-#endif
 }
 
 // 3D tiled tensor copy global -> shared (TMA engine, SASS UTMALDG): the box of

@@ -43,16 +43,11 @@ namespace sk {
 // 64 x 16 tiles, 8 stages, one 8-warp CTA per SM (212 registers, no spills):
 // 90.2 us at 256^3 against 99.4 us for the literal kernel. 64 x 32 tiles with
 // 16 warps need <= 128 registers and spill the 5-plane queues (179 us).
+// (Border pairs reading their z-neighbours from 5 live stages instead of a
+// register queue: 166 registers, 12 warps/SM with 64 x 24 tiles, 94.4 vs
+// 93.6 us -- the kernel is bound by its shared traffic; experiment removed.)
 #define SK_F2_TY 16
 #define SK_F2_S 8
-#endif
-// SK_F2_BSTAGE (experiment, off): border pairs read their z-neighbours from
-// the u stages (5 live stages) instead of a register queue, 20 fewer
-// registers; with 64 x 24 tiles that allows 12 warps per SM (166 registers,
-// 7 stages) but measured 94.4 vs 93.6 us: more warps do not help, the kernel
-// is bound by its shared-memory traffic (~100 KB per tile-plane)
-#ifndef SK_F2_BSTAGE
-#define SK_F2_BSTAGE 0
 #endif
 using CfgF2 = Cfg3<4, 64, SK_F2_TY, 2, 2, SK_F2_S, 1>;
 
@@ -123,7 +118,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
     }
     s_load = s_load + 1 == S ? 0 : s_load + 1;
   };
-  constexpr int LIVE = SK_F2_BSTAGE ? 5 : 3;  // stages read per step: k-4..k (border z from stages) or k-2..k
+  constexpr int LIVE = 3;  // stages read per step: k-2 .. k
   for (int k = 0; k < S - LIVE; ++k) issue();  // lookahead S - LIVE planes
 
   const int cofs = (2 * ty + R) * P + 2 * lane + R;    // own point (row 0, col 0) in a u stage
@@ -153,9 +148,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
   if (!has_b) b_r = cofs;  // harmless in-range offset (loads unused)
 
   double2 U[5][2], W[5][2];  // own u / w of plane j in [j % 5]: row 0 pair, row 1 pair
-#if !SK_F2_BSTAGE
   double2 UB[5];             // the border pair's u of plane j
-#endif
   int s_k = 0;               // stage of u plane k
   uint32_t fph = 0;          // parity of the current use of stage s_k
   int w_slot = 0;            // w slot of plane k-2 (written this step); plane k-4: w_slot - 2 (mod 4)
@@ -181,9 +174,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
         const double* cn = ring + s_k * PLANE;
         U[J0][0] = ld2(cn + cofs);
         U[J0][1] = ld2(cn + cofs + P);
-#if !SK_F2_BSTAGE
         UB[J0] = ld2(cn + b_r);
-#endif
       }
       const int s_k2 = s_k >= 2 ? s_k - 2 : s_k - 2 + S;  // stage of plane k-2
       // all warps past step t-1: the stage of plane k-3 and the w slot written below are free
@@ -206,14 +197,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
         *reinterpret_cast<double2*>(wsl + wofs + WP) = W[J2][1];
         if (has_b) {
           const double* c = rc + b_r;
-#if SK_F2_BSTAGE
-          auto stz = [&](int back) { return ring + (s_k >= back ? s_k - back : s_k - back + S) * PLANE + b_r; };
-          const double2 wb = l4_pair(lw, ld2(c), ld2(c - 2), ld2(c + 2), ld2(c - P), ld2(c + P), ld2(c - 2 * P),
-                                     ld2(c + 2 * P), ld2(stz(3)), ld2(stz(1)), ld2(stz(4)), ld2(stz(0)));
-#else
           const double2 wb = l4_pair(lw, UB[J2], ld2(c - 2), ld2(c + 2), ld2(c - P), ld2(c + P), ld2(c - 2 * P),
                                      ld2(c + 2 * P), UB[J3], UB[J1], UB[J4], UB[J0]);
-#endif
           *reinterpret_cast<double2*>(wsl + b_w) = wb;
         }
       }
