@@ -424,9 +424,8 @@ static bool ch_host_pipelined_ok(const sk_stencil* lap, const sk_stencil* bilap,
          is_bilap_shape(bilap, 3) && g.n[2] >= 4 * nsteps + 8 && host_pinned(c_host);
 }
 
-static int ch_host_pipelined(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
-                             double dt, int64_t nsteps, double* c_host) {
-  thread_local HostPipe hp;
+static int ch_host_pipelined_run(HostPipe& hp, const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g,
+                                 const sk_ch_params* p, double dt, int64_t nsteps, double* c_host) {
   if (int st = hp.init()) return st;
   const int64_t nz = g.n[2], plane = g.n[0] * g.n[1], S = nsteps;
   const int64_t T = 4 * S, L = nz + T;  // the unrolled line (T <= nz - 8: ch_host_pipelined_ok)
@@ -534,6 +533,17 @@ static int ch_host_pipelined(const sk_stencil* lap, const sk_stencil* bilap, con
   for (auto& m : tr) cudaEventDestroy(m.second);
 #endif
   return SK_OK;
+}
+
+static int ch_host_pipelined(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
+                             double dt, int64_t nsteps, double* c_host) {
+  thread_local HostPipe hp;
+  const int st = ch_host_pipelined_run(hp, lap, bilap, g, p, dt, nsteps, c_host);
+  if (st != SK_OK) {  // drain: no copy may still touch the caller's field after an error return
+    for (cudaStream_t s : {hp.up, hp.run, hp.down})
+      if (s) cudaStreamSynchronize(s);
+  }
+  return st;
 }
 
 }  // namespace sk
@@ -729,7 +739,10 @@ int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk
   double* sd = stage.buf + stage.elems;
   SK_CUDA_TRY(cudaMemcpyAsync(cd, c_host, n * sizeof(double), cudaMemcpyHostToDevice, hs));
   int in_scratch = 0;
-  if (int e = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, cd, sd, &in_scratch, hs)) return e;
+  if (int e = sk_ch_explicit(lap, bilap, gd, p, dt, nsteps, cd, sd, &in_scratch, hs)) {
+    cudaStreamSynchronize(hs);  // the upload may still read c_host
+    return e;
+  }
   SK_CUDA_TRY(cudaMemcpyAsync(c_host, in_scratch ? sd : cd, n * sizeof(double), cudaMemcpyDeviceToHost, hs));
   SK_CUDA_TRY(cudaStreamSynchronize(hs));
   return SK_OK;
