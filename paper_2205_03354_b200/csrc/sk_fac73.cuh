@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
     u += sg.len;
     const int64_t gx0 = sg.x0 + 2 * lane, gy0 = sg.y0 + 2 * ty;
     const bool row0 = gy0 < a.ny, row1 = gy0 + 1 < a.ny;
-    const bool vec_ok = gx0 + 2 <= a.nx;
+    const bool vec_ok = !(a.nx & 1) && gx0 + 2 <= a.nx;  // 16-byte stores: even rows (a padded input may be odd)
     double* outp = a.v + int64_t(sg.z0) * a.nx * a.ny + gy0 * a.nx + gx0;
     const int np = sg.len + 2 * R;
 
@@ -226,7 +226,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
         if (vec_ok) {
           if (row0) store_f64x2<Mode::Apply>(outp, o[0].x, o[0].y);
           if (row1) store_f64x2<Mode::Apply>(outp + a.nx, o[1].x, o[1].y);
-        }  // (bulk path only: nx even, so a pair is either whole or past the grid)
+        } else if (gx0 < a.nx) {  // odd rows (ghost-padded input): scalar stores
+          const bool x1 = gx0 + 1 < a.nx;
+          if (row0) {
+            outp[0] = o[0].x;
+            if (x1) outp[1] = o[0].y;
+          }
+          if (row1) {
+            outp[a.nx] = o[1].x;
+            if (x1) outp[a.nx + 1] = o[1].y;
+          }
+        }
         outp += a.nx * a.ny;
       }
       if (++s_k == S) {

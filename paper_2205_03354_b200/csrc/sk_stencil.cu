@@ -380,6 +380,14 @@ int launch_apply_padded(const sk_stencil* s, const GridInfo& g, const double* u_
               a.nx >= Cfg3R4P::TX + 2 * Cfg3R4P::R && a.ny >= Cfg3R4P::TY + 2 * Cfg3R4P::R &&
               plane * (a.nz + 8) < (int64_t(1) << 31);
   if (!a.bulk_ok) return kApplyPqUnsupported;
+  // B = compose(L4, L4): the padded field holds every image the assembled
+  // rows read (position-only reflections / wraps / zeros), so L4(L4 u_pad)
+  // is the assembled operator exactly in rational arithmetic, as on a
+  // periodic grid (rounding differs from the literal kernel)
+  if (is_l4l4(s) && option(SK_OPT_APPLY73_FACTORED)) {
+    const int st = launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
+    if (st != kApplyPqUnsupported) return st;
+  }
   return launch_3d<Mode::Apply, Cfg3R4P>(a, stream);
 }
 

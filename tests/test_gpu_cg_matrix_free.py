@@ -125,9 +125,42 @@ def test_padded_p_cg_is_bit_identical(sk_option, dims, bcs):
     assert g.unknown_count() == dims[0] * dims[1] * dims[2]
     b = np.sin(np.arange(g.unknown_count()) * 0.013) + 1.0
     o = SolveOptions(rel_tol=1e-9, accept_recurrence=True)
+    sk_option("apply73_factored", 0)  # the literal 73 weights on both paths (the factored apply is tested below)
     out = {}
     for flag in (1, 0):
         sk_option("cg_padded", flag)
         rep = SolveReport()
         out[flag] = (cg_solve_stencil(DeviceStencil(bilaplacian(3, 4)), g, b, o, rep), rep.iterations)
     assert np.array_equal(out[1][0], out[0][0]) and out[1][1] == out[0][1]
+
+
+@pytest.mark.parametrize("dims,bcs", [((96, 40, 30), ("clamped",) * 3), ((100, 34, 26), ("simply_supported",) * 3),
+                                      ((80, 32, 28), ("periodic", "clamped", "simply_supported"))])
+def test_padded_p_cg_factored_apply(orc, sk_option, dims, bcs):
+    # With the ghost-padded p, B = compose(L4, L4) is applied as L4(L4 p_pad)
+    # (fac73v2_kernel on the padded field): the pad holds every image the
+    # assembled rows read, so this is the assembled operator up to rounding.
+    # Same solution as the literal-weights solve and as the CSR solve of the
+    # reference-assembled matrix (oracle) to the CG parity bar.
+    from paper_2205_03354_b200.grid import GridSpec
+
+    bc = [getattr(BoundaryKind, b) for b in bcs]
+    n = [d + (2 if b != BoundaryKind.periodic else 0) for d, b in zip(dims, bc)]
+    g = GridSpec(dim=3, n=n, h=1.0 / 32, origin=[0.0] * 3, bc=bc)
+    s = bilaplacian(3, 4)
+    b = np.sin(np.arange(g.unknown_count()) * 0.013) + 1.0
+    o = SolveOptions(rel_tol=1e-10)
+    sk_option("cg_padded", 1)
+    out = {}
+    for flag in (1, 0):
+        sk_option("apply73_factored", flag)
+        rep = SolveReport()
+        out[flag] = (cg_solve_stencil(DeviceStencil(s), g, b, o, rep), rep)
+        assert rep.true_rel_residual <= 1e-10
+    (xf, rf), (xl, rl) = out[1], out[0]
+    assert np.linalg.norm(xf - xl) <= 1e-8 * np.linalg.norm(xl)
+    assert abs(rf.iterations - rl.iterations) <= max(3, 0.02 * rl.iterations)
+    rp, ci, vals = orc.assemble(s, g)
+    xo, status, its_o, _ = orc.cg_solve(rp, ci, vals, b, 1e-10)
+    assert status == 0
+    assert np.linalg.norm(xf - xo) <= 1e-8 * np.linalg.norm(xo)
