@@ -530,9 +530,10 @@ def extra_cg_matrix_free(lib, dim: int, acc: int, N: int, iters: int):
         pass
     per = ev.stop_ms() / max(rep.iterations, 1)
     # vectors only: 2D two-kernel iteration = apply (r, p in; q out) 24 + p, x, r update 56 B/row;
-    # 3D four-kernel iteration = apply 16 + p.q 16 + x, r update 48 + p update 24 B/row, + 8 B/row for the
-    # ghost-padded copy of p the radius-4 apply reads on non-periodic grids (SK_OPT_CG_PADDED)
-    per_row = 80 if dim == 2 else (112 if acc == 4 else 104)
+    # 3D radius 4 (config 5), three kernels: apply of the ghost-padded p with p.q in its epilogue 16 +
+    # x, r update 48 + p update 24 B/row + 8 B/row writing the ghost-padded copy of p
+    # (SK_OPT_CG_PADDED, SK_OPT_CG_PQ); 3D radius 2 (not run here): apply 16 + p.q 16 + 48 + 24
+    per_row = 80 if dim == 2 else (96 if acc == 4 else 104)
     bytes_it = per_row * rows
     npts = 13 if dim == 2 else 73
     return {"config": f"{2 if dim == 2 else 5}: matrix-free CG {npts}-pt clamped N={N} ({rows} rows)",
@@ -540,7 +541,8 @@ def extra_cg_matrix_free(lib, dim: int, acc: int, N: int, iters: int):
             "note": "sk_cg_solve_stencil: operator = composed stencil on the clamped grid (no matrix stream); "
                     f"roofline bytes = vectors only ({per_row} B/row/iteration"
                     + (", two kernels per iteration)" if dim == 2 else
-                       ", four kernels per iteration; p also written ghost-padded for the 16-byte loader)")}
+                       ", three kernels per iteration: the factored 73-point apply reads the ghost-padded p "
+                       "and reduces p.q in its epilogue)")}
 
 
 def extra_imex(lib, dim: int = 2, n: int = 1024, steps: int = 10, ref_steps: int = 2):

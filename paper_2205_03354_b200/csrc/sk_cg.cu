@@ -535,6 +535,10 @@ struct CgPlan {
     const int f = launch_apply_pq(op.s, op.g, p, q, st, partials, stream);  // fused p.q (3D streaming stencils)
     if (f != kApplyPqUnsupported) return f;
     if (padded) {
+      if (option(SK_OPT_CG_PQ)) {  // fused p.q (factored 73-point apply on the padded p)
+        const int e = launch_apply_padded(op.s, op.g, ppad + pl.at(0, 0, 0), pl.px, pl.plane, q, stream, st, partials);
+        if (e != kApplyPqUnsupported) return e;
+      }
       if (int e = launch_apply_padded(op.s, op.g, ppad + pl.at(0, 0, 0), pl.px, pl.plane, q, stream)) return e;
     } else if (int e = launch_apply(op.s, op.g, p, q, stream)) {
       return e;

@@ -82,9 +82,18 @@ __device__ __forceinline__ double2 l4_pair(const L4W& lw, double2 c, double2 l, 
   return make_double2(fma(lw.a2, s2a, fma(lw.a1, s1a, lw.a0 * c.x)), fma(lw.a2, s2b, fma(lw.a1, s1b, lw.a0 * c.y)));
 }
 
-template <class C>
+// PQ (matrix-free CG on the ghost-padded p, sk_cg.cu): q = A p with p.q
+// reduced in the store epilogue from the register queue (u(k-4) is p at the
+// output point) and alpha published by the last CTA; the separate p.q pass
+// disappears. A no-op once the solver has stopped.
+template <class C, bool PQ = false>
 __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, const L4W lw) {
   constexpr int R = 4, S = C::STAGES, P = C::PITCH, PLANE = C::PLANE;
+  if constexpr (PQ) {
+    if (a.cg->status != kCgRunning) return;
+  }
+  double pq = 0.0;
+  (void)pq;
   static_assert(C::R == 4 && C::PX == 2 && C::PY == 2 && C::TX == 64, "layout: warp = row pair");
   using SM = F2Smem<C>;
   constexpr int WP = SM::WP, WPLANE = SM::WPLANE, WS = SM::WSLOTS;
@@ -237,6 +246,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
             if (x1) outp[a.nx + 1] = o[1].y;
           }
         }
+        if constexpr (PQ) {  // p at the output points: the centre of u plane k-4 (J4)
+          const bool x0ok = gx0 < a.nx, x1ok = gx0 + 1 < a.nx;
+          if (row0) {
+            if (x0ok) pq = fma(U[J4][0].x, o[0].x, pq);
+            if (x1ok) pq = fma(U[J4][0].y, o[0].y, pq);
+          }
+          if (row1) {
+            if (x0ok) pq = fma(U[J4][1].x, o[1].x, pq);
+            if (x1ok) pq = fma(U[J4][1].y, o[1].y, pq);
+          }
+        }
         outp += a.nx * a.ny;
       }
       if (++s_k == S) {
@@ -260,6 +280,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) fac73v2_kernel(const Args3D a, 
     }
   }
   cp_async_wait_all();
+  if constexpr (PQ) {
+    __shared__ double sh[32];
+    pq = block_sum<C::THREADS>(pq, sh);
+    if (threadIdx.x == 0) a.cg_partials[blockIdx.x] = pq;
+    if (last_block(&a.cg->counter[0])) {
+      const double t = reduce_partials<C::THREADS>(a.cg_partials, gridDim.x, sh);
+      if (threadIdx.x == 0) cg_publish_pq(a.cg, t);
+    }
+  }
 }
 
 }  // namespace sk

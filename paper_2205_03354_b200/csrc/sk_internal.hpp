@@ -95,8 +95,11 @@ int launch_apply(const sk_stencil* s, const GridInfo& g, const double* u, double
 // the same apply from a ghost-padded field (radius-4 3D stencils; sk_cg.cu's
 // PadLayout): kApplyPqUnsupported when not applicable
 bool apply_padded_supported(const sk_stencil* s, const GridInfo& g);
+// st != nullptr: q = A p fused with p.q -> alpha (kApplyPqUnsupported when the
+// kernel for this stencil has no fused form)
 int launch_apply_padded(const sk_stencil* s, const GridInfo& g, const double* u_origin, int64_t pitch,
-                        int64_t plane, double* v, cudaStream_t stream);
+                        int64_t plane, double* v, cudaStream_t stream, CgState* st = nullptr,
+                        double* partials = nullptr);
 
 // Fused matrix-free CG half-iteration on a 2D class-1 stencil (Mode::CgApply):
 // q = A p' with p' = r + beta p formed on the load, alpha from p'.q.

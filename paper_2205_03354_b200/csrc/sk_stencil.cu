@@ -286,12 +286,13 @@ static bool is_l4l4(const sk_stencil* s) {
 // axis +-1: 16/12, axis +-2: -1/12, generators.cpp:98) scaled by h^-2 per
 // pass. 16-byte periodic path only (whole-tile halos, even nx); returns
 // kApplyPqUnsupported when the grid needs the literal kernel instead.
+template <bool PQ = false>
 static int launch_fac73(Args3D a, double h_m2, cudaStream_t stream) {
   using C = CfgF2;
   using SM = F2Smem<C>;
   if (!a.bulk_ok || a.nx < C::TX + 2 * C::R || a.ny < C::TY + 2 * C::R) return kApplyPqUnsupported;
   const L4W lw{(3.0 * (-30.0 / 12.0)) * h_m2, (16.0 / 12.0) * h_m2, (-1.0 / 12.0) * h_m2};
-  auto kern = fac73v2_kernel<C>;
+  auto kern = fac73v2_kernel<C, PQ>;
   static int once = set_smem(kern, SM::BYTES);
   if (once != SK_OK) return once;
   a.zrot = 1;
@@ -362,8 +363,9 @@ bool apply_padded_supported(const sk_stencil* s, const GridInfo& g) {
 }
 
 int launch_apply_padded(const sk_stencil* s, const GridInfo& g, const double* u_origin, int64_t pitch,
-                        int64_t plane, double* v, cudaStream_t stream) {
+                        int64_t plane, double* v, cudaStream_t stream, CgState* st, double* partials) {
   if (!apply_padded_supported(s, g)) return kApplyPqUnsupported;
+  const bool pq = st != nullptr;
   const double scale = pow_int(g.h, s->h_power);
   Args3D a{};
   a.u = u_origin;
@@ -385,9 +387,13 @@ int launch_apply_padded(const sk_stencil* s, const GridInfo& g, const double* u_
   // is the assembled operator exactly in rational arithmetic, as on a
   // periodic grid (rounding differs from the literal kernel)
   if (is_l4l4(s) && option(SK_OPT_APPLY73_FACTORED)) {
-    const int st = launch_fac73(a, pow_int(g.h, s->h_power / 2), stream);
-    if (st != kApplyPqUnsupported) return st;
+    a.cg = st;
+    a.cg_partials = partials;
+    const int r = pq ? launch_fac73<true>(a, pow_int(g.h, s->h_power / 2), stream)
+                     : launch_fac73<false>(a, pow_int(g.h, s->h_power / 2), stream);
+    if (r != kApplyPqUnsupported) return r;
   }
+  if (pq) return kApplyPqUnsupported;  // the literal radius-4 kernel has no fused p.q (registers)
   return launch_3d<Mode::Apply, Cfg3R4P>(a, stream);
 }
 
