@@ -7,6 +7,8 @@ from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, make_grid
 from paper_2205_03354_b200.linalg import SolveOptions, cg_solve_stencil
 from paper_2205_03354_b200.stencil import bilaplacian
 lib = _lib.ensure_device(0)
+if "unrolled" in sys.argv:  # unrolled iteration graphs: ncu cannot profile kernel nodes under conditional nodes
+    _lib.set_option("cg_device_loop", 0)
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 dim = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 acc = 2 if dim == 2 else 4
