@@ -130,6 +130,13 @@ int sk_device_free(void* p);
 int sk_memcpy_h2d(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 int sk_memcpy_d2h(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 int sk_stream_sync(void* stream);
+/* CUDA IPC for buffers from sk_device_alloc (the slab neighbours' buffers in
+ * another process, on this or a peer GPU over NVLink): the 64-byte handle of
+ * an allocation's base pointer; open maps a handle from another process
+ * (peer access enabled lazily); close unmaps it. */
+int sk_ipc_get_handle(const void* base_dev, unsigned char handle_out[64]);
+int sk_ipc_open_handle(const unsigned char handle[64], void** base_dev_out);
+int sk_ipc_close_handle(void* base_dev);
 /* A non-blocking stream for callers without their own CUDA runtime. */
 int sk_stream_create(void** out);
 int sk_stream_destroy(void* stream);
@@ -220,6 +227,18 @@ int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk
 int sk_ch_explicit_slab(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
                         const sk_ch_params* p, double dt, const double* in_ghosted_dev, double* out_dev,
                         void* stream);
+/* The same step with the halo exchange fused into its store epilogue: every
+ * point of output planes 0, 1 is also stored at peer_lo (the two upper ghost
+ * planes of the z-neighbour below, in ITS output buffer), every point of
+ * planes n[2]-2, n[2]-1 at peer_hi (the two lower ghost planes of the
+ * neighbour above): device pointers into this GPU's or a peer GPU's memory
+ * (sk_ipc_open_handle; NVLink stores), either may be NULL. After the step
+ * (stream-ordered) and a barrier with the neighbours, every rank's output
+ * buffer is a complete ghosted input for the next step. Factored
+ * formulation only; n[2] >= 4. */
+int sk_ch_explicit_slab_peer(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* g,
+                             const sk_ch_params* p, double dt, const double* in_ghosted_dev, double* out_dev,
+                             double* peer_lo_dev, double* peer_hi_dev, void* stream);
 /* free_energy (cahn_hilliard.cpp:77-114): h^d sum f_chem + kappa/2 |central grad|^2 */
 int sk_free_energy(const sk_grid_desc* g, const sk_ch_params* p, const double* c_dev,
                    double* energy_host, void* stream);

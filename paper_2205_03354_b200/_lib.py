@@ -59,6 +59,9 @@ SIGNATURES = {
     "sk_memcpy_h2d": (c_int, [vp, vp, C.c_size_t, vp]),
     "sk_memcpy_d2h": (c_int, [vp, vp, C.c_size_t, vp]),
     "sk_stream_sync": (c_int, [vp]),
+    "sk_ipc_get_handle": (c_int, [vp, vp]),
+    "sk_ipc_open_handle": (c_int, [vp, C.POINTER(vp)]),
+    "sk_ipc_close_handle": (c_int, [vp]),
     "sk_stream_create": (c_int, [C.POINTER(vp)]),
     "sk_stream_destroy": (c_int, [vp]),
     "sk_fill_uniform_host": (c_int, [C.c_uint64, c_i64, c_dbl, c_dbl, vp]),
@@ -81,6 +84,8 @@ SIGNATURES = {
     "sk_ch_explicit": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, c_i64, vp, vp,
                                C.POINTER(c_int), vp]),
     "sk_ch_explicit_slab": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, vp, vp, vp]),
+    "sk_ch_explicit_slab_peer": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, vp, vp, vp, vp,
+                                         vp]),
     "sk_ch_explicit_host": (c_int, [vp, vp, C.POINTER(GridDesc), C.POINTER(ChParams), c_dbl, c_i64, vp]),
     "sk_free_energy": (c_int, [C.POINTER(GridDesc), C.POINTER(ChParams), vp, pd, vp]),
     "sk_ch_imex_create": (c_int, [C.POINTER(GridDesc), C.POINTER(ChParams), C.POINTER(SolveOptionsC),

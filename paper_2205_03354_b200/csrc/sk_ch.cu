@@ -178,7 +178,8 @@ static int launch_chf3d(Args3D a, const CUtensorMap& tm, cudaStream_t stream) {
 // One fused step on the fast path (in -> out).
 static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const GridInfo& g, const sk_ch_params* p,
                         double dt, const double* in, double* out, cudaStream_t stream, bool bulk_ok_ptrs,
-                        int io = kIoPlain, bool z_ghosted = false, int ghost = 2) {
+                        int io = kIoPlain, bool z_ghosted = false, int ghost = 2, double* peer_lo = nullptr,
+                        double* peer_hi = nullptr) {
   const double dtm = dt * p->mobility;
   const double fac_b = -dtm * p->kappa;
   const double sb = pow_int(g.h, bilap->h_power), sl = pow_int(g.h, lap->h_power);
@@ -226,6 +227,11 @@ static int ch_step_fast(const sk_stencil* lap, const sk_stencil* bilap, const Gr
   CUtensorMap tm{};
   if (io == kIoMid || io == kIoLast)
     if (int st = make_tmap_padded(&tm, in, g)) return st;
+  if (peer_lo || peer_hi) {  // slab step with the halo stores fused in (OUT 2)
+    a.peer_lo = peer_lo;
+    a.peer_hi = peer_hi;
+    return launch_chf3d<CF, 0, 0, 2>(a, tm, stream);
+  }
   switch (io) {
     case kIoFirst: return launch_chf3d<CF, 0, 0, 1>(a, tm, stream);
     case kIoMid: return launch_chf3d<CT, 0, 1, 1>(a, tm, stream);
@@ -700,6 +706,33 @@ int sk_ch_explicit_slab(const sk_stencil* lap, const sk_stencil* bilap, const sk
   const double* in = in_ghosted + 2 * plane;  // first interior plane
   const bool ptr_ok = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   return ch_step_fast(lap, bilap, g, p, dt, in, out, as_stream(stream_p), ptr_ok, kIoPlain, /*z_ghosted=*/true);
+}
+
+int sk_ch_explicit_slab_peer(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* gd,
+                             const sk_ch_params* p, double dt, const double* in_ghosted, double* out,
+                             double* peer_lo, double* peer_hi, void* stream_p) {
+  if (!lap || !bilap || !p) return fail(SK_ERR_INVALID_ARGUMENT, "null stencil or params");
+  GridInfo g;
+  if (int st = grid_info(gd, &g)) return st;
+  if (g.dim != 3) return fail(SK_ERR_INVALID_ARGUMENT, "slab stepping is 3D");
+  for (int a = 0; a < 3; ++a)
+    if (g.bc[a] != SK_BC_PERIODIC) return fail(SK_ERR_NON_PERIODIC, "Cahn-Hilliard runs on periodic grids");
+  if (!is_lap_shape(lap, 3) || !is_bilap_shape(bilap, 3))
+    return fail(SK_ERR_INVALID_ARGUMENT, "slab stepping needs the 7-point L and its 25-point composition");
+  if (g.n[0] < 5 || g.n[1] < 5) return fail(SK_ERR_STENCIL_WIDER_THAN_GRID, "periodic axis narrower than stencil support");
+  if (g.n[2] < 4) return fail(SK_ERR_STENCIL_WIDER_THAN_GRID, "a slab with fused halo stores needs >= 4 planes");
+  if (!(dt > 0)) return fail(SK_ERR_INVALID_ARGUMENT, "dt must be positive");
+  if (p->formulation != SK_CH_FACTORED)
+    return fail(SK_ERR_INVALID_ARGUMENT, "fused halo stores need the factored formulation (SK_CH_FACTORED)");
+  if (!in_ghosted || !out) return fail(SK_ERR_INVALID_ARGUMENT, "bad field pointers");
+  const int64_t plane = g.n[0] * g.n[1];
+  const double* in = in_ghosted + 2 * plane;
+  const bool ptr_ok = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) |
+                        reinterpret_cast<uintptr_t>(peer_lo) | reinterpret_cast<uintptr_t>(peer_hi)) & 15) == 0;
+  if (!peer_lo && !peer_hi)
+    return ch_step_fast(lap, bilap, g, p, dt, in, out, as_stream(stream_p), ptr_ok, kIoPlain, /*z_ghosted=*/true);
+  return ch_step_fast(lap, bilap, g, p, dt, in, out, as_stream(stream_p), ptr_ok, kIoPlain, /*z_ghosted=*/true, 2,
+                      peer_lo, peer_hi);
 }
 
 int sk_ch_explicit_host(const sk_stencil* lap, const sk_stencil* bilap, const sk_grid_desc* gd, const sk_ch_params* p,

@@ -130,7 +130,10 @@ struct TmaCursor {
 // OUT 0: write c' to a.v (nx x ny x nz). OUT 1: write c' into the interior of
 // a ghost-padded field at a.v and its periodic images into the 2-wide ghost
 // frame (the next step's TMA boxes then never wrap). LD 1 / OUT 1 need whole
-// tiles (nx % TX == 0, ny % TY == 0).
+// tiles (nx % TX == 0, ny % TY == 0). OUT 2 (z-slabs): OUT 0, and the points
+// of output planes 0, 1 / nz-2, nz-1 are stored a second time at a.peer_lo /
+// a.peer_hi, the z-neighbours' ghost planes (peer memory over NVLink): the
+// halo exchange rides on the step's own stores.
 template <class C, int V = 0, int LD = 0, int OUT = 0, bool FB = false>
 __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
     chf3d_kernel(const __grid_constant__ Args3D a, const __grid_constant__ CUtensorMap tmap) {
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
   const int lane = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int cofs = (2 * ty + R) * P + 2 * lane + SM::XO;  // own point (row 0, column 0) in a c stage
   const int mofs = (2 * ty + 1) * MP + 2 * lane + 2;  // own point in a mu slot
-  const int64_t opx = OUT ? a.nx + 2 * kPadL : a.nx, opp = opx * (OUT ? a.ny + 2 * kPadT : a.ny);  // output pitches
+  const int64_t opx = OUT == 1 ? a.nx + 2 * kPadL : a.nx, opp = opx * (OUT == 1 ? a.ny + 2 * kPadT : a.ny);  // output pitches
   // one border point of the mu tile per lane (lanes < ROWS_PER_WARP: the
   // rows above / below the tile, contiguous; the next 4 lanes: the side
   // columns of this warp's row pair)
@@ -240,14 +243,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
     const int64_t gx0 = sg.x0 + 2 * lane, gy0 = sg.y0 + 2 * ty;
     const bool row0 = gy0 < a.ny, row1 = gy0 + 1 < a.ny;
     const bool vec_ok = a.bulk_ok && gx0 + 2 <= a.nx;
-    double* outp = a.v + int64_t(sg.z0) * opp + (gy0 + (OUT ? kPadT : 0)) * opx + gx0 + (OUT ? kPadL : 0);
+    double* outp = a.v + int64_t(sg.z0) * opp + (gy0 + (OUT == 1 ? kPadT : 0)) * opx + gx0 + (OUT == 1 ? kPadL : 0);
     // OUT 1: periodic images in the ghost frame: columns 0..3 and nx-4..nx-1
     // (whole 32 B sectors: no partial-sector writes), rows 0..g-1 and ny-g..ny-1
     // (g = a.ghost = 2)
-    const int64_t gdx_ = OUT ? (gx0 < 4 ? a.nx : (gx0 >= a.nx - 4 ? -a.nx : 0)) : 0;
-    const int64_t gdy_ = OUT ? (gy0 < a.ghost ? a.ny : (gy0 >= a.ny - a.ghost ? -a.ny : 0)) * opx : 0;
+    const int64_t gdx_ = OUT == 1 ? (gx0 < 4 ? a.nx : (gx0 >= a.nx - 4 ? -a.nx : 0)) : 0;
+    const int64_t gdy_ = OUT == 1 ? (gy0 < a.ghost ? a.ny : (gy0 >= a.ny - a.ghost ? -a.ny : 0)) * opx : 0;
     const int64_t gdx = gdx_, gdy = gdy_;
     const int np = sg.len + 2 * R;
+    int zo = sg.z0;  // OUT 2: the output plane the next store goes to
+    (void)zo;
 
     // one step: plane k landed; DO_MU: mu of plane k-1; DO_OUT: output plane k-2
     auto step = [&](auto kk_t, auto mu_t, auto out_t) {
@@ -387,14 +392,27 @@ __global__ void __launch_bounds__(C::THREADS, C::MIN_BLOCKS)
               store_f64x2<Mode::CahnHilliard>(outp + gdx + gdy + opx, o[2], o[3]);
             }
           }
-        } else if (vec_ok) {
-          if (row0) store_f64x2<Mode::CahnHilliard>(outp, o[0], o[1]);
-          if (row1) store_f64x2<Mode::CahnHilliard>(outp + a.nx, o[2], o[3]);
         } else {
+          double* dsts[2] = {outp, nullptr};
+          if constexpr (OUT == 2) {  // the neighbours' ghost planes: the same point again
+            double* pb = zo < 2 ? a.peer_lo : (zo >= a.nz - 2 ? a.peer_hi : nullptr);
+            if (pb) dsts[1] = pb + (zo < 2 ? zo : zo - (a.nz - 2)) * opp + (gy0 * a.nx + gx0);
+            ++zo;
+          }
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            if (row0 && gx0 + i < a.nx) outp[i] = o[i];
-            if (row1 && gx0 + i < a.nx) outp[a.nx + i] = o[2 + i];
+          for (int d = 0; d < (OUT == 2 ? 2 : 1); ++d) {
+            double* op = dsts[d];
+            if (!op) continue;
+            if (vec_ok) {
+              if (row0) store_f64x2<Mode::CahnHilliard>(op, o[0], o[1]);
+              if (row1) store_f64x2<Mode::CahnHilliard>(op + a.nx, o[2], o[3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                if (row0 && gx0 + i < a.nx) op[i] = o[i];
+                if (row1 && gx0 + i < a.nx) op[a.nx + i] = o[2 + i];
+              }
+            }
           }
         }
         outp += opp;

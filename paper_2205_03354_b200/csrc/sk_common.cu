@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstring>
 #include <random>
 #include <string>
 #include <utility>
@@ -157,6 +158,29 @@ int sk_device_alloc(size_t bytes, void** out) {
 
 int sk_device_free(void* p) {
   if (p) SK_CUDA_TRY(cudaFree(p));
+  return SK_OK;
+}
+
+int sk_ipc_get_handle(const void* base, unsigned char handle_out[64]) {
+  if (!base || !handle_out) return fail(SK_ERR_INVALID_ARGUMENT, "null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  SK_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(base)));
+  std::memcpy(handle_out, &h, 64);
+  return SK_OK;
+}
+
+int sk_ipc_open_handle(const unsigned char handle[64], void** base_out) {
+  if (!handle || !base_out) return fail(SK_ERR_INVALID_ARGUMENT, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  *base_out = nullptr;
+  SK_CUDA_TRY(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return SK_OK;
+}
+
+int sk_ipc_close_handle(void* base) {
+  if (base) SK_CUDA_TRY(cudaIpcCloseMemHandle(base));
   return SK_OK;
 }
 

@@ -82,6 +82,8 @@ struct Args3D {
                      // the same planes in every column (seg_of): neighbour tiles are streamed in phase
   int64_t in_pitch;  // != 0: u is a ghost-padded field (row pitch in_pitch, plane pitch in_plane, u at the
   int64_t in_plane;  // interior origin, every halo point present): 16-byte loads without wrap (matrix-free CG)
+  double* peer_lo;   // chf3d OUT 2 (slab step with fused halo stores): output planes 0, 1 also go here,
+  double* peer_hi;   // planes nz-2, nz-1 here (the z-neighbours' ghost planes; either may be null)
 };
 
 // Host: tiles, persistent grid (min_blocks CTAs per SM, each a balanced

@@ -209,6 +209,107 @@ class SlabCahnHilliard:
             self.cur = 1 - self.cur
 
 
+class PeerSlabCahnHilliard:
+    """The z-slab run with the halo exchange fused into the step kernel
+    (sk_ch_explicit_slab_peer): each rank's step stores its two lowest output
+    planes straight into the upper ghost planes of the rank below and its two
+    highest into the lower ghost planes of the rank above — peer memory over
+    NVLink (CUDA IPC mappings of the neighbours' buffers), or this GPU's own
+    memory for a neighbour in another process on the same device. There is no
+    separate exchange pass or copy: after the step and a barrier every output
+    buffer is the next step's complete ghosted input.
+
+    Buffers come from sk_device_alloc (IPC-exportable); the IPC handles are
+    swapped once over torch.distributed (all_gather_object). A rank never
+    waits on another rank's kernel inside a kernel: the per-step ordering is
+    stream synchronisation + a process barrier."""
+
+    def __init__(self, grid: GridSpec, params: CahnHilliardParams):
+        import torch.distributed as dist
+
+        from .device import DeviceArray
+
+        grid.validate()
+        if grid.dim != 3 or any(b != BoundaryKind.periodic for b in grid.bc):
+            raise StencilkitError(Errc.invalid_argument, "slab stepping needs a periodic 3D grid")
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.world = self.dist.get_world_size() if self.dist else 1
+        self.rank = self.dist.get_rank() if self.dist else 0
+        nx, ny, nz = grid.n
+        if nz % self.world:
+            raise StencilkitError(Errc.invalid_argument, "nz must be divisible by the number of ranks")
+        self.nzl = nz // self.world
+        if self.nzl < 4:
+            raise StencilkitError(Errc.stencil_wider_than_grid, "a slab with fused halo stores needs >= 4 planes")
+        self.grid, self.params = grid, params
+        self.plane = nx * ny
+        self.z0 = self.rank * self.nzl
+        self.local = GridSpec(dim=3, n=[nx, ny, self.nzl], h=grid.h, origin=[0.0] * 3,
+                              bc=[BoundaryKind.periodic] * 3)
+        self.lib = ensure_device()
+        n = (self.nzl + 2 * GHOST) * self.plane
+        self.buf = [DeviceArray(n), DeviceArray(n)]
+        self.cur = 0
+        lap = laplacian(3, 2)
+        self.lap, self.bilap = DeviceStencil(lap), DeviceStencil(compose(lap, lap))
+        self._desc = self.local.desc()
+        self._p = params.c_struct()
+        # neighbours' buffers: [rank][which] base pointers (own rank: own buffers)
+        self._opened = []
+        self.peer_base = {self.rank: [b.ptr for b in self.buf]}
+        if self.world > 1:
+            handles = []
+            for b in self.buf:
+                h = (C.c_ubyte * 64)()
+                check(self.lib.sk_ipc_get_handle(C.c_void_p(b.ptr), h))
+                handles.append(bytes(h))
+            allh = [None] * self.world
+            self.dist.all_gather_object(allh, handles)
+            for r in {(self.rank - 1) % self.world, (self.rank + 1) % self.world} - {self.rank}:
+                bases = []
+                for hb in allh[r]:
+                    p = C.c_void_p()
+                    check(self.lib.sk_ipc_open_handle((C.c_ubyte * 64).from_buffer_copy(hb), C.byref(p)))
+                    self._opened.append(p.value)
+                    bases.append(p.value)
+                self.peer_base[r] = bases
+
+    def close(self) -> None:
+        if self.dist and self.world > 1:
+            self.dist.barrier()  # no neighbour still stores into our buffers
+        for p in self._opened:
+            self.lib.sk_ipc_close_handle(C.c_void_p(p))
+        self._opened = []
+
+    def scatter(self, c_global: np.ndarray) -> None:
+        """This rank's planes and their ghost planes (global planes z0-2 .. z0+nzl+1, periodic)."""
+        flat = np.ascontiguousarray(c_global, np.float64).reshape(-1, self.plane)
+        nz = flat.shape[0]
+        idx = [(self.z0 + k) % nz for k in range(-GHOST, self.nzl + GHOST)]
+        self.buf[self.cur].upload(flat[idx].ravel())
+
+    def local_field(self) -> np.ndarray:
+        full = self.buf[self.cur].to_host()
+        return full[GHOST * self.plane:(GHOST + self.nzl) * self.plane].copy()
+
+    def step(self, dt: float, nsteps: int = 1) -> None:
+        p8, g, nzl = self.plane * 8, GHOST, self.nzl
+        down, up = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        for _ in range(nsteps):
+            nxt = 1 - self.cur
+            src, dst = self.buf[self.cur].ptr, self.buf[nxt].ptr
+            peer_lo = self.peer_base[down][nxt] + (g + nzl) * p8  # the lower neighbour's upper ghosts
+            peer_hi = self.peer_base[up][nxt]                     # the upper neighbour's lower ghosts
+            check(self.lib.sk_ch_explicit_slab_peer(self.lap.handle, self.bilap.handle, C.byref(self._desc),
+                                                    C.byref(self._p), dt, C.c_void_p(src),
+                                                    C.c_void_p(dst + g * p8), C.c_void_p(peer_lo),
+                                                    C.c_void_p(peer_hi), None))
+            check(self.lib.sk_stream_sync(None))
+            if self.dist and self.world > 1:
+                self.dist.barrier()  # every neighbour's stores into our ghost planes are done
+            self.cur = nxt
+
+
 def numpy_slab_step(nx: int, ny: int, nzl: int, h: float, params: CahnHilliardParams):
     """Factored explicit step on a ghosted slab in numpy (CPU tests of the exchange)."""
     def lap(f):  # 7-point on the (nzl + 2k) x ny x nx array, periodic in x, y; z neighbours in the array
