@@ -1,0 +1,164 @@
+"""The reference's own unit-test cases for this path, replayed through the GPU
+library (assembly, SpMV and csr_matmul on the device, the matrix-free apply).
+
+Each test names the case of /root/reference/proj/tests/unit it restates; the
+assertions and tolerances are the reference's (one bound corrected: see the sine-mode
+test). Inputs are generated here
+(seeded numpy / python RNGs in place of std::mt19937 where the draw itself is
+not the point)."""
+import math
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from paper_2205_03354_b200.errors import StencilkitError
+from paper_2205_03354_b200.grid import (BoundaryKind, GridSpec, apply, assemble, composed_apply, csr_matmul,
+                                        make_grid, make_periodic_grid)
+from paper_2205_03354_b200.stencil import Stencil, StencilSpec, builtin_stencil, compose, from_entries, laplacian, make
+
+pytestmark = pytest.mark.gpu
+
+
+def dense(m):
+    rp, ci, v = m.to_host()
+    d = np.zeros((m.rows, m.cols))
+    for i in range(m.rows):
+        for k in range(rp[i], rp[i + 1]):
+            d[i, ci[k]] = v[k]
+    return d
+
+
+def csr_close(a, b, rel):
+    """test_grid.cpp:30-39: same pattern, values within rel * max|a|."""
+    ra, ca, va = a.to_host()
+    rb, cb, vb = b.to_host()
+    if a.rows != b.rows or a.cols != b.cols or a.nnz() != b.nnz():
+        return False
+    if not (np.array_equal(ra, rb) and np.array_equal(ca, cb)):
+        return False
+    return bool(np.all(np.abs(va - vb) <= rel * np.abs(va).max()))
+
+
+def random_stencil(rng: random.Random, dim: int, max_support: int) -> Stencil:
+    """test_util.hpp:17-33: 1-5 entries, offsets in [-s, s], numerators in [-6, 6] \\ {0}, denominators 1-4,
+    h power in [-2, 0]."""
+    entries = {}
+    for _ in range(rng.randint(1, 5)):
+        off = tuple(rng.randint(-max_support, max_support) for _ in range(dim))
+        n = rng.randint(-6, 6) or 1
+        entries[off] = Fraction(n, rng.randint(1, 4))
+    return from_entries(dim, rng.randint(-2, 0), entries.items())
+
+
+def test_apply_constants_identity_and_shape_checks():
+    # test_grid.cpp:97-111
+    g = make_periodic_grid(2, 16, 1.0)
+    lap = assemble(laplacian(2, 2), g)
+    assert np.all(np.abs(apply(lap, np.full(lap.rows, 3.25))) <= 1e-13)
+    eye = assemble(Stencil.identity(2), g)
+    x = np.random.default_rng(5).uniform(-1, 1, eye.rows)
+    assert np.array_equal(apply(eye, x), x)
+    with pytest.raises(StencilkitError):
+        apply(eye, np.zeros(eye.rows + 1))
+    # the matrix-free apply agrees on the same inputs
+    assert np.all(np.abs(composed_apply(laplacian(2, 2), g, np.full(g.unknown_count(), 3.25))) <= 1e-13)
+    assert np.array_equal(composed_apply(Stencil.identity(2), g, x), x)
+
+
+def test_second_derivative_acts_as_its_symbol_on_a_sine_mode():
+    # test_grid.cpp:113-131
+    n = 64
+    h = 1.0 / n
+    g = make_periodic_grid(1, n, h)
+    s = make(StencilSpec(2, 2))
+    m = assemble(s, g)
+    lam = (2.0 * math.cos(2 * math.pi * h) - 2.0) / (h * h)  # symbol of [1, -2, 1] at theta = 2 pi h
+    v = np.sin(2 * math.pi * np.arange(n) * h)
+    # second-order agreement with -(2 pi)^2 sin: the reference states the bound
+    # as 50 h^2, below the scheme's own leading error |lam + 4 pi^2| =
+    # 16 pi^4 h^2 / 12 + O(h^4) ~ 130 h^2 (= 0.0317 here); asserted with that constant
+    bound = 16 * math.pi ** 4 / 12 * h * h * 1.001 + 1e-10
+    for got in (apply(m, v), composed_apply(s, g, v)):
+        assert np.all(np.abs(got - lam * v) <= 1e-12 * abs(lam))
+        assert np.all(np.abs(got + 4 * math.pi ** 2 * v) <= bound)
+
+
+def test_composing_before_assembly_matches_multiplying_assembled_operators():
+    # test_grid.cpp:133-143 (GPU assembly and GPU csr_matmul)
+    rng = random.Random(2024)
+    for trial in range(8):
+        dim = 1 + trial % 2
+        a, b = random_stencil(rng, dim, 2), random_stencil(rng, dim, 2)
+        g = make_periodic_grid(dim, 11, 0.5)
+        product = csr_matmul(assemble(b, g), assemble(a, g))
+        direct = assemble(compose(a, b), g)
+        assert csr_close(direct, product, 1e-13), trial
+
+
+def test_periodic_fourier_modes_map_through_the_symbol():
+    # test_grid.cpp:145-163
+    n = 16
+    g = make_periodic_grid(2, n, 2.0)
+    lap = laplacian(2, 2)
+    m = assemble(lap, g)
+    j, i = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    for kx in (0, 1, 5):
+        for ky in (0, 3):
+            tx, ty = 2 * math.pi * kx / n, 2 * math.pi * ky / n
+            lam = ((2 * math.cos(tx) - 2) + (2 * math.cos(ty) - 2)) / (g.h * g.h)
+            v = np.cos(tx * i + ty * j).ravel()
+            for got in (apply(m, v), composed_apply(lap, g, v)):
+                assert np.all(np.abs(got - lam * v) <= 1e-10 * (abs(lam) + 1.0))
+
+
+def test_simply_supported_odd_reflection_squares_the_dirichlet_laplacian():
+    # test_grid.cpp:165-172
+    g = make_grid(2, 17, 1.0 / 16, BoundaryKind.simply_supported)
+    lap = laplacian(2, 2)
+    lap_d = assemble(lap, g)
+    assert csr_close(assemble(compose(lap, lap), g), csr_matmul(lap_d, lap_d), 1e-13)
+
+
+def test_simply_supported_1d_second_derivative_is_the_dirichlet_tridiagonal():
+    # test_grid.cpp:174-187
+    g = GridSpec(dim=1, n=[6], h=1.0, origin=[0.0], bc=[BoundaryKind.simply_supported])
+    m = assemble(make(StencilSpec(2, 2)), g)
+    assert m.rows == 4 and m.nnz() == 4 + 2 * 3
+    rp, ci, v = m.to_host()
+    for r in range(m.rows):
+        for k in range(rp[r], rp[r + 1]):
+            assert v[k] == (-2.0 if ci[k] == r else 1.0)
+
+
+def test_stencil_wider_than_the_grid_is_rejected():
+    # test_grid.cpp:189-200
+    wide = compose(builtin_stencil("dxx-dxx"), builtin_stencil("dxx-dxx"))  # support 8
+    with pytest.raises(StencilkitError):
+        assemble(wide, make_periodic_grid(1, 8, 1.0))
+    with pytest.raises(StencilkitError):
+        composed_apply(wide, make_periodic_grid(1, 8, 1.0), np.zeros(8))
+    g = GridSpec(dim=1, n=[3], h=1.0, origin=[0.0], bc=[BoundaryKind.simply_supported])
+    with pytest.raises(StencilkitError):
+        assemble(builtin_stencil("wide-heat"), g)  # needs |offset| <= n - 2
+
+
+def test_grid_validation():
+    # test_grid.cpp:202-212
+    with pytest.raises(StencilkitError):
+        GridSpec(dim=2, n=[4], h=1.0, origin=[0.0, 0.0], bc=[BoundaryKind.periodic] * 2).validate()
+    with pytest.raises(StencilkitError):
+        make_periodic_grid(1, 2, 1.0)  # too few points
+    with pytest.raises(StencilkitError):
+        assemble(Stencil.identity(2), make_periodic_grid(1, 8, 1.0))  # dimension mismatch
+
+
+def test_csr_matmul_agrees_with_dense_arithmetic():
+    # test_linalg.cpp:147-174 (the csr_matmul half; identity_plus_scaled is covered by the IMEX tests)
+    g = make_periodic_grid(1, 8, 1.0)
+    lap = assemble(make(StencilSpec(2, 2)), g)
+    dl = dense(lap)
+    dp = dense(csr_matmul(lap, lap))
+    want = dl @ dl
+    assert np.all(np.abs(dp - want) <= 1e-14 * np.maximum(np.abs(want), 1e-300))
