@@ -138,12 +138,13 @@ __global__ void k3_xpby(int64_t n, const double* __restrict__ r, double* __restr
 // the image -x-2 when x < R and 2un-x when x >= un-R (periodic: x+un / x-un).
 struct PadLayout {
   int pad = 0;         // frame width (>= R + 1, even)
+  int padx = 0;        // frame width before x = 0 (>= pad): 16 puts every interior row on a 128-byte boundary
   int64_t px = 0, py = 0, plane = 0;  // row and plane pitch (elements)
   int64_t un[3] = {0, 0, 0};
   int bc[3] = {0, 0, 0};
   int R = 4;
   __host__ __device__ int64_t at(int64_t x, int64_t y, int64_t z) const {
-    return (z + pad) * plane + (y + pad) * px + (x + pad);
+    return (z + pad) * plane + (y + pad) * px + (x + padx);
   }
 };
 
@@ -726,7 +727,11 @@ int cg_plan_create(const CgOperator& op, int check_every, cudaStream_t stream, C
       L.un[a] = op.g.un[a];
       L.bc[a] = op.g.bc[a];
     }
-    L.px = (op.g.un[0] + 2 * L.pad + 1) / 2 * 2;
+    // interior rows start 128-byte aligned (whole-line stores from the p update;
+    // the apply's 16-byte tile loads stay aligned): 16 columns before x = 0,
+    // >= pad after the last, the pitch a multiple of 16
+    L.padx = 16;
+    L.px = (L.padx + op.g.un[0] + L.pad + 15) / 16 * 16;
     L.py = op.g.un[1] + 2 * L.pad;
     L.plane = L.px * L.py;
     const size_t elems = size_t(L.plane) * size_t(op.g.un[2] + 2 * L.pad);
