@@ -162,3 +162,28 @@ def test_csr_matmul_agrees_with_dense_arithmetic():
     dp = dense(csr_matmul(lap, lap))
     want = dl @ dl
     assert np.all(np.abs(dp - want) <= 1e-14 * np.maximum(np.abs(want), 1e-300))
+
+
+def test_cg_edge_cases():
+    # linalg.cpp:15-25: shape checks, and a zero right-hand side returns x = 0 without iterating
+    from paper_2205_03354_b200.errors import Errc
+    from paper_2205_03354_b200.linalg import SolveOptions, SolveReport, cg_solve, cg_solve_stencil
+    from paper_2205_03354_b200.stencil import bilaplacian
+
+    g = make_grid(2, 17, 1.0 / 16, BoundaryKind.clamped)
+    s = bilaplacian(2)
+    m = assemble(s, g)
+    for solve in (lambda b, r: cg_solve(m, b, SolveOptions(rel_tol=1e-10), r),
+                  lambda b, r: cg_solve_stencil(s, g, b, SolveOptions(rel_tol=1e-10), r)):
+        rep = SolveReport()
+        x = solve(np.zeros(m.rows), rep)
+        assert np.array_equal(x, np.zeros(m.rows)) and rep.iterations == 0
+        with pytest.raises(StencilkitError) as e:
+            solve(np.ones(m.rows + 1), SolveReport())
+        assert e.value.code == Errc.shape_mismatch
+    from paper_2205_03354_b200.grid import CsrMatrix
+
+    tall = CsrMatrix.upload(np.array([0, 1, 2, 3]), np.array([0, 1, 0]), np.array([1.0, 1.0, 1.0]), cols=2)
+    with pytest.raises(StencilkitError) as e:
+        cg_solve(tall, np.ones(3))
+    assert e.value.code == Errc.shape_mismatch
