@@ -167,8 +167,13 @@ __device__ __forceinline__ int pad_images(const PadLayout& L, int a, int64_t x, 
 // one interior point (x, y, z) with value v: its padded position and images
 __device__ __forceinline__ void pad_store(const PadLayout& L, double* __restrict__ pp, int64_t x, int64_t y,
                                           int64_t z, bool row_edge, double v) {
-  if (!row_edge && x >= L.R && x < L.un[0] - L.R) {
+  if (!row_edge) {  // a row away from the y / z faces: images along x only
     pp[L.at(x, y, z)] = v;
+    if (x >= L.R && x < L.un[0] - L.R) return;
+    int64_t px[3];
+    double sx[3];
+    const int nx = pad_images(L, 0, x, px, sx);
+    for (int a = 1; a < nx; ++a) pp[L.at(px[a], y, z)] = sx[a] * v;
     return;
   }
   int64_t px[3], py[3], pz[3];
