@@ -57,3 +57,36 @@ def test_random_stencil_parity(orc, seed):
     got = composed_apply(s, g, u)
     scale = max(float(np.abs(want).max()), 1e-300)
     assert float(np.abs(got - want).max()) <= 1e-12 * scale, seed
+
+
+def ch_case(seed):
+    rng = random.Random(1000 + seed)
+    dim = 2 + seed % 2
+    if dim == 2:
+        dims = [rng.choice([rng.randint(5, 40), rng.randint(64, 140)]) for _ in range(2)]
+    else:
+        dims = [rng.choice([rng.randint(5, 20), 64, rng.randint(65, 90)]), rng.choice([rng.randint(5, 20), 16, 32, 48]),
+                rng.randint(5, 24)]
+    steps = rng.choice([1, 2, 3, rng.randint(4, 30), 101, 102])
+    form = rng.choice(["factored", "composed"])
+    return dims, steps, form
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_ch_parity(orc, seed):
+    # explicit CH on random periodic grids (partial and whole tiles, z extents
+    # down to 5, chunk boundaries at 101 / 102 steps), both formulations, vs the
+    # oracle's restated step (cahn_hilliard.cpp:146-152) at the 1e-9 bar
+    from paper_2205_03354_b200.cahn_hilliard import CahnHilliardExplicit, CahnHilliardParams, CahnHilliardState
+
+    dims, steps, form = ch_case(seed)
+    dim = len(dims)
+    p = CahnHilliardParams.from_epsilon(0.02, form)
+    h = 1.0 / max(dims)
+    dt = (0.2 * h ** 4 / (144 * p.kappa)) if dim == 3 else (0.25 * h ** 4 / (64 * p.kappa))
+    g = GridSpec(dim=dim, n=dims, h=h, origin=[0.0] * dim, bc=[BoundaryKind.periodic] * dim)
+    c0 = 0.05 * np.random.default_rng(seed).uniform(-1, 1, g.unknown_count())
+    st = CahnHilliardState(g, c0.copy())
+    CahnHilliardExplicit(g, p).step(st, dt, steps)
+    ref = orc.ch_explicit_dims(dims, h, p, dt, steps, c0)
+    assert np.linalg.norm(st.c - ref) / np.linalg.norm(ref) <= 1e-9, (dims, steps, form)
