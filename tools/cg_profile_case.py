@@ -6,6 +6,10 @@ from paper_2205_03354_b200.errors import StencilkitError
 from paper_2205_03354_b200.grid import BoundaryKind, DeviceStencil, make_grid
 from paper_2205_03354_b200.linalg import SolveOptions, cg_solve_stencil
 from paper_2205_03354_b200.stencil import bilaplacian
+if "--lib" in sys.argv:  # an A/B build (tools/ab_build.py)
+    from pathlib import Path
+
+    _lib.load(Path(sys.argv[sys.argv.index("--lib") + 1]))
 lib = _lib.ensure_device(0)
 if "unrolled" in sys.argv:  # unrolled iteration graphs: ncu cannot profile kernel nodes under conditional nodes
     _lib.set_option("cg_device_loop", 0)
