@@ -506,7 +506,8 @@ struct CgPlan {
   bool padded = false;
   PadLayout pl;
   double* ppad = nullptr;
-  int kernels_per_iteration() const { return fused2d ? 2 : ((op.m || pq_fused) ? 3 : 4); }
+  int kpi = 0;  // kernels one iteration launches (counted while capturing)
+  int kernels_per_iteration() const { return kpi ? kpi : (fused2d ? 2 : ((op.m || pq_fused) ? 3 : 4)); }
 
   ~CgPlan() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -603,10 +604,13 @@ struct CgPlan {
     device_loop = false;
     SK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     int st_ = SK_OK;
+    const int64_t l0 = g_launches.load();
     for (int k = 0; k < check_every && st_ == SK_OK; ++k) st_ = iteration(x, cap, false, 0);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap, &graph);
-    g_launches -= int64_t(kernels_per_iteration()) * check_every;  // capture does not execute
+    const int64_t captured = g_launches.load() - l0;
+    if (st_ == SK_OK && check_every > 0) kpi = int(captured / check_every);
+    g_launches -= captured;  // capture does not execute
     if (st_ != SK_OK) {
       if (graph) cudaGraphDestroy(graph);
       return st_;
@@ -648,6 +652,7 @@ struct CgPlan {
     }
     if (int e = launch_q(cap)) return e;
     k2_update_rr<false, false><<<grid, kT, 0, cap>>>(n, p, q, x, r, st, partials, h);
+    SK_LAUNCH_CHECK("k2_update_rr");
     if (padded) {
       if (cond)
         k3_xpby_pad<true><<<pad_grid(), 256, 0, cap>>>(r, p, ppad, pl, st, h);
@@ -658,6 +663,7 @@ struct CgPlan {
     } else {
       k3_xpby<false><<<grid, kT, 0, cap>>>(n, r, p, st, h);
     }
+    SK_LAUNCH_CHECK("k3_xpby");
     return SK_OK;
   }
   int build_loop_graph(double* x, cudaStream_t cap) {
@@ -683,10 +689,13 @@ struct CgPlan {
     // body: kLoopUnroll iterations (no-ops once the status leaves RUNNING),
     // the last one publishing the loop condition
     int st_ = SK_OK;
+    const int64_t l0 = g_launches.load();
     for (int k = 0; k < kLoopUnroll && st_ == SK_OK; ++k) st_ = iteration(x, cap, k + 1 == kLoopUnroll, h);
     cudaGraph_t out = nullptr;
     const cudaError_t e = cudaStreamEndCapture(cap, &out);
-    g_launches -= int64_t(kernels_per_iteration()) * kLoopUnroll;  // capture does not execute
+    const int64_t captured = g_launches.load() - l0;
+    if (st_ == SK_OK) kpi = int(captured / kLoopUnroll);
+    g_launches -= captured;  // capture does not execute
     if (st_ != SK_OK || e != cudaSuccess) return SK_ERR_CUDA;
     if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
       exec = nullptr;
