@@ -22,6 +22,7 @@
 
 #include <sk_cuda.h>
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -307,6 +308,94 @@ class CahnHilliardExplicit {
 #include "stencilkit/generators.hpp"
 
 inline stencilkit::Stencil stencilkit::cuda::CahnHilliardExplicit::laplacian_of(const GridSpec& g) {
+  return laplacian(g.dim, 2);
+}
+
+namespace stencilkit::cuda {
+/// One rank's z-slab of a periodic 3D explicit Cahn-Hilliard run across GPUs
+/// (one process per GPU). `slab` is the local grid (n[2] =
+/// this rank's interior planes, n[0], n[1] the full x / y extents). Its two
+/// ghosted buffers (n[2] + 4 planes) come from sk_device_alloc, so they are
+/// IPC-exportable: handles() gives their 64-byte handles for the caller's
+/// communicator (MPI_Allgather, ...), connect() maps the z-neighbours'
+/// (connect_self() for a single rank), and step() runs one fused step whose
+/// store epilogue also writes the two boundary planes into the neighbours'
+/// ghost planes (NVLink peer stores; sk_ch_explicit_slab_peer). After each
+/// step the caller puts a barrier between the ranks (the stream is
+/// synchronised inside step()).
+class SlabStepper {
+ public:
+  using Handle = std::array<unsigned char, 64>;
+  SlabStepper(const GridSpec& slab, const CahnHilliardParams& p)
+      : desc_(grid_desc(slab)), params_(ch_params(p, SK_CH_FACTORED)), plane_(slab.n[0] * slab.n[1]),
+        nz_(slab.n[2]), lap_(laplacian_of(slab)), bilap_(compose(laplacian_of(slab), laplacian_of(slab))) {
+    for (auto& b : buf_) check(sk_device_alloc(bytes(), reinterpret_cast<void**>(&b)));
+  }
+  ~SlabStepper() {
+    for (double* q : opened_) sk_ipc_close_handle(q);
+    for (double* b : buf_) sk_device_free(b);
+  }
+  SlabStepper(const SlabStepper&) = delete;
+  SlabStepper& operator=(const SlabStepper&) = delete;
+
+  std::array<Handle, 2> handles() const {
+    std::array<Handle, 2> h{};
+    for (int i = 0; i < 2; ++i) check(sk_ipc_get_handle(buf_[i], h[i].data()));
+    return h;
+  }
+  void connect(const std::array<Handle, 2>& lower, const std::array<Handle, 2>& upper) {
+    for (int i = 0; i < 2; ++i) {
+      lower_[i] = open(lower[i]);
+      upper_[i] = open(upper[i]);
+    }
+  }
+  void connect_self() {  // a single rank: the ghosts are its own
+    for (int i = 0; i < 2; ++i) lower_[i] = upper_[i] = buf_[i];
+  }
+  /// this rank's interior planes and the two ghost planes on each side (z-major)
+  void load(std::span<const double> ghosted) {
+    if (static_cast<std::int64_t>(ghosted.size()) != (nz_ + 4) * plane_)
+      throw Error(Errc::shape_mismatch, "ghosted slab size");
+    check(sk_memcpy_h2d(buf_[cur_], ghosted.data(), bytes(), nullptr));
+    check(sk_stream_sync(nullptr));
+  }
+  void step(double dt) {
+    const int nxt = 1 - cur_;
+    double* peer_lo = lower_[nxt] + (2 + nz_) * plane_;  // the lower neighbour's upper ghost planes
+    double* peer_hi = upper_[nxt];                       // the upper neighbour's lower ghost planes
+    check(sk_ch_explicit_slab_peer(lap_.get(), bilap_.get(), &desc_, &params_, dt, buf_[cur_],
+                                   buf_[nxt] + 2 * plane_, peer_lo, peer_hi, nullptr));
+    check(sk_stream_sync(nullptr));
+    cur_ = nxt;
+  }
+  std::vector<double> interior() const {
+    std::vector<double> out(static_cast<size_t>(nz_ * plane_));
+    check(sk_memcpy_d2h(out.data(), buf_[cur_] + 2 * plane_, out.size() * sizeof(double), nullptr));
+    return out;
+  }
+
+ private:
+  static Stencil laplacian_of(const GridSpec& g);
+  size_t bytes() const { return static_cast<size_t>((nz_ + 4) * plane_) * sizeof(double); }
+  double* open(const Handle& h) {
+    void* p = nullptr;
+    check(sk_ipc_open_handle(h.data(), &p));
+    opened_.push_back(static_cast<double*>(p));
+    return static_cast<double*>(p);
+  }
+  sk_grid_desc desc_;
+  sk_ch_params params_;
+  std::int64_t plane_, nz_;
+  DeviceStencil lap_, bilap_;
+  double* buf_[2] = {nullptr, nullptr};
+  double* lower_[2] = {nullptr, nullptr};
+  double* upper_[2] = {nullptr, nullptr};
+  std::vector<double*> opened_;
+  int cur_ = 0;
+};
+}  // namespace stencilkit::cuda
+
+inline stencilkit::Stencil stencilkit::cuda::SlabStepper::laplacian_of(const GridSpec& g) {
   return laplacian(g.dim, 2);
 }
 
