@@ -314,7 +314,8 @@ inline stencilkit::Stencil stencilkit::cuda::CahnHilliardExplicit::laplacian_of(
 namespace stencilkit::cuda {
 /// One rank's z-slab of a periodic 3D explicit Cahn-Hilliard run across GPUs
 /// (one process per GPU). `slab` is the local grid (n[2] =
-/// this rank's interior planes, n[0], n[1] the full x / y extents). Its two
+/// this rank's interior planes, the same on every rank, >= 4; n[0], n[1] the
+/// full x / y extents). Its two
 /// ghosted buffers (n[2] + 4 planes) come from sk_device_alloc, so they are
 /// IPC-exportable: handles() gives their 64-byte handles for the caller's
 /// communicator (MPI_Allgather, ...), connect() maps the z-neighbours'
@@ -329,7 +330,16 @@ class SlabStepper {
   SlabStepper(const GridSpec& slab, const CahnHilliardParams& p)
       : desc_(grid_desc(slab)), params_(ch_params(p, SK_CH_FACTORED)), plane_(slab.n[0] * slab.n[1]),
         nz_(slab.n[2]), lap_(laplacian_of(slab)), bilap_(compose(laplacian_of(slab), laplacian_of(slab))) {
-    for (auto& b : buf_) check(sk_device_alloc(bytes(), reinterpret_cast<void**>(&b)));
+    if (slab.dim != 3 || nz_ < 4) throw Error(Errc::invalid_argument, "a 3D slab of at least 4 planes");
+    for (auto& b : buf_) {
+      void* q = nullptr;
+      const int st = sk_device_alloc(bytes(), &q);
+      if (st != SK_OK) {
+        for (double* d : buf_) sk_device_free(d);
+        check(st);
+      }
+      b = static_cast<double*>(q);
+    }
   }
   ~SlabStepper() {
     for (double* q : opened_) sk_ipc_close_handle(q);
