@@ -246,9 +246,20 @@ int launch_generic(const sk_stencil* s, const GridInfo& g, const double* u, doub
   }
   a.scale = pow_int(g.h, s->h_power);
   a.rows = g.rows;
+  for (int d = 0; d < 3; ++d) {
+    a.lo[d] = d < g.dim ? s->lo[d] : 0;
+    a.hi[d] = d < g.dim ? s->hi[d] : 0;
+  }
   if (g.rows == 0) return SK_OK;
+  if (g.un[1] > 65535 || g.un[2] > 65535)
+    return fail(SK_ERR_INVALID_ARGUMENT, "generic apply: more than 65535 unknowns along y or z");
   const int threads = 256;
-  stencil_generic_kernel<<<unsigned((g.rows + threads - 1) / threads), threads, 0, stream>>>(a);
+  const size_t smem = size_t(s->nent) * 16;
+  static int once = set_smem(stencil_generic_kernel, 227 * 1024);
+  if (once != SK_OK) return once;
+  if (smem > 227 * 1024) return fail(SK_ERR_INVALID_ARGUMENT, "generic apply: too many stencil entries");
+  const dim3 grid(unsigned((g.un[0] + threads - 1) / threads), unsigned(g.un[1]), unsigned(g.un[2]));
+  stencil_generic_kernel<<<grid, threads, smem, stream>>>(a);
   SK_LAUNCH_CHECK("stencil_generic_kernel");
   return SK_OK;
 }

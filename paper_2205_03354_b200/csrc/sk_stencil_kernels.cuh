@@ -325,9 +325,13 @@ __global__ void __launch_bounds__(Tile2D<TX, TY, PX, PY>::THREADS)
 
 // =========================================================================
 // Generic fallback: any stencil (dim 1..3, any offsets, any boundary kind),
-// one thread per unknown, entries read through the read-only cache. Row
-// semantics follow assemble (grid.cpp:89-138): periodic wrap, odd (simply
-// supported) or even (clamped) reflection, boundary ghosts dropped.
+// one thread per unknown. Row semantics follow assemble (grid.cpp:89-138):
+// periodic wrap, odd (simply supported) or even (clamped) reflection,
+// boundary ghosts dropped. Launched over (x blocks, y, z), so the point's
+// index needs no division; every entry's linear offset and weight sit in
+// shared memory, and a point whose whole support lies inside the grid
+// (no wrap, no reflection) sums u[row + delta_e] directly. Entries are summed
+// in stencil order on both paths (the same bits as the boundary logic).
 // =========================================================================
 struct GenericArgs {
   const double* __restrict__ u;
@@ -340,18 +344,35 @@ struct GenericArgs {
   int bc[3];
   double scale;  // pow_int(h, h_power)
   int64_t rows;
+  int lo[3], hi[3];  // the stencil's support per axis
 };
 
-static __global__ void stencil_generic_kernel(const GenericArgs a) {
-  const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= a.rows) return;
-  int64_t idx[3];
-  int64_t rem = row;
-  for (int d = 0; d < 3; ++d) {
-    idx[d] = rem % a.un[d];
-    rem /= a.un[d];
+static __global__ void __launch_bounds__(256) stencil_generic_kernel(const GenericArgs a) {
+  extern __shared__ __align__(16) unsigned char gen_smem[];
+  int64_t* delta = reinterpret_cast<int64_t*>(gen_smem);  // linear offset of each entry
+  double* wv = reinterpret_cast<double*>(delta + a.nent);  // its weight (coeff * h^power)
+  for (int e = threadIdx.x; e < a.nent; e += blockDim.x) {
+    int64_t dl = 0, stride = 1;
+    for (int d = 0; d < a.dim; ++d) {
+      dl += stride * __ldg(a.off + 3 * e + d);
+      stride *= a.un[d];
+    }
+    delta[e] = dl;
+    wv[e] = __ldg(a.coeff + e) * a.scale;
   }
+  __syncthreads();
+  const int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= a.un[0]) return;
+  const int64_t idx[3] = {x, int64_t(blockIdx.y), int64_t(blockIdx.z)};
+  const int64_t row = x + a.un[0] * (idx[1] + a.un[1] * idx[2]);
+  bool inner = true;
+  for (int d = 0; d < a.dim; ++d) inner = inner && idx[d] + a.lo[d] >= 0 && idx[d] + a.hi[d] <= a.un[d] - 1;
   double acc = 0.0;
+  if (inner) {
+    for (int e = 0; e < a.nent; ++e) acc = fma(wv[e], __ldg(a.u + row + delta[e]), acc);
+    a.v[row] = acc;
+    return;
+  }
   for (int e = 0; e < a.nent; ++e) {
     double val = __ldg(a.coeff + e) * a.scale;
     int64_t col = 0, stride = 1;
